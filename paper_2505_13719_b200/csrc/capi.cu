@@ -1,0 +1,900 @@
+// C-ABI of libcuhallar.so (include/cuhallar.h): instance upload, persistent
+// kernel launch, host <-> device layout conversion.  Host orchestration only;
+// all solver arithmetic runs in hallar_kernel (solve.cuh).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/cuhallar.h"
+#include "host_instances.hpp"
+#include "solve.cuh"
+
+using namespace hallar;
+namespace hh = hallar_host;
+
+// ----------------------------------------------------------------- kernel ---
+namespace hallar {
+__global__ void __launch_bounds__(kThreads, 1)
+    hallar_kernel(const __grid_constant__ Params P, SolveOut* so) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  Ctx c;
+  c.t.rank = blockIdx.x;
+  c.t.size = gridDim.x;
+  c.t.bar = P.bar;
+  c.t.slots = P.slots;
+  c.t.epoch = 0;
+  c.t.parity = 0;
+  c.warp = threadIdx.x >> 5;
+  c.lane = threadIdx.x & 31;
+  double* sm = reinterpret_cast<double*>(smem_raw);
+  c.rs.part = sm;
+  sm += kWarps * kRedK;
+  c.rs.out = sm;
+  sm += kRedK;
+  c.tile = sm + c.warp * kTile * kTileLd;
+  sm += kWarps * kTile * kTileLd;
+  c.cs = sm;
+  sm += kSMax;
+  c.H = sm;
+  sm += kHLd * kHLd;
+  c.JA = sm;
+  sm += 32 * 32;
+  c.JV = sm;
+  sm += 32 * 32;
+  c.E = sm;
+  sm += 32 * 32;
+  c.ev = sm;
+  sm += 32;
+  c.jcs = sm;
+  sm += 32;
+  c.hh = sm;
+  sm += 32;
+  c.hh2 = sm;
+  sm += 32;
+  c.vsum = sm;
+  sm += 64;
+  int* ip = reinterpret_cast<int*>(sm);
+  c.col = ip;
+  ip += 40;
+  c.jpq = ip;
+  c.rl = row_split(P.I, c.t.rank, c.t.size);
+  c.rh = row_split(P.I, c.t.rank + 1, c.t.size);
+  c.kl = P.I.np * c.t.rank / c.t.size;
+  c.kh = P.I.np * (c.t.rank + 1) / c.t.size;
+  if (P.op == kOpSolve) {
+    solve_dev(c, P, so);
+  } else {
+    HALLAR_DISPATCH_S(P.s_in, op_dispatch<S_>(c, P, so));
+  }
+}
+
+// column-major (ld) <-> row-major (stride s) factor conversion
+__global__ void to_rowmajor(const double* __restrict__ src, int64_t ld, int s, int64_t n,
+                            double* __restrict__ dst) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= n * s) return;
+  const int64_t a = t / s, k = t % s;
+  dst[t] = src[a + k * ld];
+}
+__global__ void to_colmajor(const double* __restrict__ src, int s, int64_t n, double* dst,
+                            int64_t ld) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= n * s) return;
+  const int64_t a = t % n, k = t / n;
+  dst[a + k * ld] = src[a * s + k];
+}
+// lower-order copy of an edge-order vector: dst[e] = src[eid[e]]
+__global__ void gather_lower(const double* __restrict__ src, const int64_t* __restrict__ eid,
+                             int64_t cnt, double* __restrict__ dst) {
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e < cnt) dst[e] = src[eid[e]];
+}
+}  // namespace hallar
+
+namespace {
+
+thread_local std::string g_err;
+
+constexpr size_t kSmemBytes =
+    sizeof(double) * (kWarps * kRedK + kRedK + kWarps * kTile * kTileLd + kSMax + kHLd * kHLd +
+                      3 * 32 * 32 + 4 * 32 + 64) +
+    sizeof(int) * 80;
+
+struct CudaError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+void ck(cudaError_t e, const char* what) {
+  if (e != cudaSuccess)
+    throw CudaError(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+template <class T>
+T* dalloc(size_t count, int64_t* acct) {
+  if (count == 0) count = 1;
+  void* p = nullptr;
+  ck(cudaMalloc(&p, count * sizeof(T)), "cudaMalloc");
+  if (acct) *acct += int64_t(count * sizeof(T));
+  return static_cast<T*>(p);
+}
+template <class T>
+T* dupload(const std::vector<T>& v, int64_t* acct) {
+  T* p = dalloc<T>(v.size(), acct);
+  if (!v.empty()) ck(cudaMemcpy(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice), "H2D");
+  return p;
+}
+
+int grid_size(int requested) {
+  static int cached = -1;
+  if (cached < 0) {
+    ck(cudaFuncSetAttribute(hallar_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            int(kSmemBytes)),
+       "smem attr");
+    int dev = 0, sms = 0, per = 0;
+    ck(cudaGetDevice(&dev), "device");
+    ck(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev), "sm count");
+    ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, hallar_kernel, kThreads, kSmemBytes),
+       "occupancy");
+    if (per < 1) throw CudaError("hallar_kernel cannot be resident");
+    cached = sms * per;
+  }
+  if (requested > 0) return std::min(requested, cached);
+  return cached;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------- instance ---
+struct cuhallar_instance {
+  hh::HostInst h;
+  DevPairs I{};
+  int64_t bytes = 0;
+  std::vector<int64_t> lo_eid_host;
+  // device arrays
+  int32_t *ei = nullptr, *ej = nullptr, *lo_col = nullptr;
+  int64_t *up_ptr = nullptr, *lo_ptr = nullptr, *lo_eid = nullptr;
+  double *b_up = nullptr, *b_lo = nullptr;
+  // workspace
+  int ws_grid = 0;
+  unsigned long long* bar = nullptr;
+  double* slots = nullptr;
+  double* buf[kNBuf] = {};
+  double* vslot = nullptr;
+  int nslot = 0;
+  double *p_up = nullptr, *p_lo = nullptr, *q_up = nullptr, *q_lo = nullptr, *r_up = nullptr,
+         *r_lo = nullptr;
+  double* lz_rand = nullptr;
+  int n_refill = 0;
+  uint64_t lz_seed = ~0ull;
+  double* dscal = nullptr;
+  int* discal = nullptr;
+  SolveOut* dso = nullptr;
+  TraceEv* trace_host = nullptr;
+  int* trace_count_host = nullptr;
+  int trace_cap = 4096;
+  std::mutex mu;
+
+  ~cuhallar_instance() {
+    auto f = [](void* p) {
+      if (p) cudaFree(p);
+    };
+    f(ei); f(ej); f(lo_col); f(up_ptr); f(lo_ptr); f(lo_eid); f(b_up); f(b_lo);
+    f(bar); f(slots); for (auto* b : buf) f(b); f(vslot);
+    f(p_up); f(p_lo); f(q_up); f(q_lo); f(r_up); f(r_lo); f(lz_rand); f(dscal); f(discal); f(dso);
+    if (trace_host) cudaFreeHost(trace_host);
+    if (trace_count_host) cudaFreeHost(trace_count_host);
+  }
+};
+
+struct cuhallar_solution {
+  int64_t n = 0, m = 0;
+  int rank = 0;
+  std::vector<double> U;  // column-major
+  std::vector<double> p;
+};
+
+namespace {
+
+// Upload the pair structure and build the lower CSR (stable by edge id).
+void upload_pairs(cuhallar_instance* in) {
+  auto& h = in->h;
+  const int64_t n = h.n, np = h.np;
+  std::vector<int64_t> up(n + 1, 0), lo(n + 1, 0);
+  for (int64_t k = 0; k < np; ++k) {
+    ++up[h.ei[k] + 1];
+    ++lo[h.ej[k] + 1];
+  }
+  for (int64_t a = 0; a < n; ++a) {
+    up[a + 1] += up[a];
+    lo[a + 1] += lo[a];
+  }
+  std::vector<int32_t> lo_col(np);
+  std::vector<int64_t> lo_eid(np);
+  {
+    std::vector<int64_t> cur(lo.begin(), lo.end() - 1);
+    for (int64_t k = 0; k < np; ++k) {
+      const int64_t e = cur[h.ej[k]]++;
+      lo_col[e] = h.ei[k];
+      lo_eid[e] = k;
+    }
+  }
+  in->ei = dupload(h.ei, &in->bytes);
+  in->ej = dupload(h.ej, &in->bytes);
+  in->up_ptr = dupload(up, &in->bytes);
+  in->lo_ptr = dupload(lo, &in->bytes);
+  in->lo_col = dupload(lo_col, &in->bytes);
+  in->lo_eid = dupload(lo_eid, &in->bytes);
+  in->lo_eid_host = std::move(lo_eid);
+  DevPairs& I = in->I;
+  I.family = h.family;
+  I.has_trace = h.has_trace ? 1 : 0;
+  I.n = n;
+  I.np = np;
+  I.m = h.m;
+  I.ei = in->ei;
+  I.ej = in->ej;
+  I.up_ptr = in->up_ptr;
+  I.lo_ptr = in->lo_ptr;
+  I.lo_col = in->lo_col;
+  I.lo_eid = in->lo_eid;
+  // scale_instance (solver.cpp:31-42): b <- b / tau, norm_b1 <- norm_b1 / tau
+  std::vector<double> bs(h.m);
+  for (int64_t k = 0; k < h.m; ++k) bs[k] = h.tau != 1.0 ? h.b[k] / h.tau : h.b[k];
+  I.norm_b1 = h.tau != 1.0 ? h.norm_b1 / h.tau : h.norm_b1;
+  I.nb2 = std::sqrt(hh::eigen_order_sum_sq(bs.data(), h.m));
+  I.norm_C1 = h.norm_C1;
+  if (h.has_trace) {
+    I.b_trace = bs[h.m - 1];
+    bool any = false;
+    for (int64_t k = 0; k < np; ++k) any |= bs[k] != 0.0;
+    if (any) throw hh::InputError("theta: nonzero edge right-hand side");
+  } else {
+    std::vector<double> bl(np);
+    for (int64_t e = 0; e < np; ++e) bl[e] = bs[in->lo_eid_host[e]];
+    bs.resize(np);
+    in->b_up = dupload(bs, &in->bytes);
+    in->b_lo = dupload(bl, &in->bytes);
+    I.b_up = in->b_up;
+    I.b_lo = in->b_lo;
+  }
+}
+
+void ensure_workspace(cuhallar_instance* in, int grid, uint64_t seed, int block_restart) {
+  const int64_t n = in->h.n, np = in->h.np;
+  if (!in->bar) {
+    in->bar = dalloc<unsigned long long>(1, &in->bytes);
+    for (auto& b : in->buf) b = dalloc<double>(size_t(n) * kSMax, &in->bytes);
+    in->p_up = dalloc<double>(np, &in->bytes);
+    in->p_lo = dalloc<double>(np, &in->bytes);
+    in->q_up = dalloc<double>(np, &in->bytes);
+    in->q_lo = dalloc<double>(np, &in->bytes);
+    in->r_up = dalloc<double>(np, &in->bytes);
+    in->r_lo = dalloc<double>(np, &in->bytes);
+    in->dscal = dalloc<double>(8, &in->bytes);
+    in->discal = dalloc<int>(8, &in->bytes);
+    in->dso = dalloc<SolveOut>(1, &in->bytes);
+    ck(cudaHostAlloc(&in->trace_host, sizeof(TraceEv) * in->trace_cap, cudaHostAllocMapped),
+       "trace ring");
+    ck(cudaHostAlloc(&in->trace_count_host, sizeof(int), cudaHostAllocMapped), "trace count");
+  }
+  if (grid > in->ws_grid) {
+    if (in->slots) cudaFree(in->slots);
+    in->slots = dalloc<double>(size_t(2) * grid * kRedK, &in->bytes);
+    in->ws_grid = grid;
+  }
+  const int kmax = int(std::min<int64_t>(block_restart, n));
+  const int need = kmax + std::max(1, kmax / 3) + 8;
+  if (need > in->nslot) {
+    if (in->vslot) cudaFree(in->vslot);
+    in->vslot = dalloc<double>(size_t(n) * need, &in->bytes);
+    in->nslot = need;
+  }
+  if (seed != in->lz_seed) {
+    // Lanczos start vector + breakdown refills: the stream of
+    // gaussian_vector(n, Rng(seed ^ 0x9b97f4a7c15)) calls (lanczos.cpp:46-50, 128-129)
+    const int refill = int(std::max<int64_t>(2, std::min<int64_t>(64, (int64_t(1) << 24) / n)));
+    const auto v = hh::gaussian_stream(seed ^ 0x9b97f4a7c15ULL, n * (1 + refill));
+    if (in->lz_rand) cudaFree(in->lz_rand);
+    in->lz_rand = dupload(v, &in->bytes);
+    in->n_refill = refill;
+    in->lz_seed = seed;
+  }
+}
+
+Cfg to_dev_cfg(const cuhallar_config& c) {
+  Cfg d{};
+  d.eps = c.eps;
+  d.beta0 = c.beta0;
+  d.beta_growth = c.beta_growth;
+  d.eps0 = c.eps0;
+  d.eps_decay = c.eps_decay;
+  d.eps_floor = c.eps_floor;
+  d.max_outer = c.max_outer;
+  d.time_limit = c.time_limit;
+  d.eig_tol = c.eig_tol;
+  d.eig_max_iters = c.eig_max_iters;
+  d.eig_block_restart = c.eig_block_restart;
+  d.aipp_lambda0 = c.aipp_lambda0;
+  d.aipp_rho = c.aipp_rho;
+  d.aipp_max_outer = c.aipp_max_outer;
+  d.aipp_lambda_underflow = c.aipp_lambda_underflow;
+  d.fista_sigma = c.fista_sigma;
+  d.fista_chi = c.fista_chi;
+  d.fista_mu = c.fista_mu;
+  d.fista_L0 = c.fista_L0;
+  d.fista_max_iters = c.fista_max_iters;
+  d.max_fw_steps = c.max_fw_steps;
+  d.trace = c.trace;
+  return d;
+}
+
+void validate_cfg(const cuhallar_config& c) {
+  auto need = [](bool ok, const char* w) {
+    if (!ok) throw hh::InputError(w);
+  };
+  need(c.eps > 0, "config: eps must be positive");
+  need(c.beta_growth >= 1.0, "config: beta_growth must be >= 1");
+  need(c.eps_decay > 0 && c.eps_decay <= 1.0, "config: eps_decay in (0,1]");
+  need(c.max_outer >= 1, "config: max_outer must be >= 1");
+  need(c.time_limit > 0, "config: time_limit must be positive");
+  need(c.max_fw_steps >= 1, "config: max_fw_steps must be >= 1");
+  need(c.eig_tol > 0, "eig: tol must be positive");
+  need(c.eig_block_restart >= 2, "eig: block_restart must be >= 2");
+  need(c.eig_block_restart <= kLanczosMax, "eig: block_restart above the device cap (32)");
+  need(c.eig_max_iters >= c.eig_block_restart, "eig: max_iters < block_restart");
+  need(c.aipp_lambda0 > 0, "aipp: lambda0 must be positive");
+  need(c.aipp_max_outer >= 1, "aipp: max_outer must be >= 1");
+  need(c.fista_sigma > 0 && c.fista_sigma < 0.5, "fista: sigma must lie in (0, 1/2)");
+  need(c.fista_chi > 0 && c.fista_chi < 1, "fista: chi must lie in (0, 1)");
+  need(c.fista_mu > 0, "fista: mu must be positive");
+}
+
+const char* msg_text(int id) {
+  switch (id) {
+    case kMsgFistaDiverged: return "fista: curvature estimate diverged";
+    case kMsgAlValue: return "al_value: non-finite result";
+    case kMsgAlValGrad: return "AlFunction::value_and_gradient: non-finite result";
+    case kMsgAlGrad: return "al_gradient: non-finite result";
+    case kMsgGradOp: return "gradient_operator: non-finite multiplier";
+    case kMsgProjectBall: return "project_ball: non-finite input";
+    case kMsgNonFinite: return "non-finite iterate";
+    case kMsgRankCap: return "factor rank exceeds the device cap (32)";
+    case kMsgRefillCap: return "lanczos: breakdown refill / slot capacity exceeded";
+    case kMsgRank32: return "factor rank above 32 is not supported";
+    default: return "";
+  }
+}
+
+Params base_params(cuhallar_instance* in, const cuhallar_config* cfg) {
+  Params P;
+  P.I = in->I;
+  cuhallar_config dc;
+  cuhallar_config_default(&dc);
+  P.cfg = to_dev_cfg(cfg ? *cfg : dc);
+  P.bar = in->bar;
+  P.slots = in->slots;
+  for (int i = 0; i < kNBuf; ++i) P.buf[i] = in->buf[i];
+  P.vslot = in->vslot;
+  P.nslot = in->nslot;
+  P.lz_rand = in->lz_rand;
+  P.n_refill = in->n_refill;
+  P.p_up = in->p_up;
+  P.p_lo = in->p_lo;
+  P.q_up = in->q_up;
+  P.q_lo = in->q_lo;
+  P.r_up = in->r_up;
+  P.r_lo = in->r_lo;
+  P.scalars = in->dscal;
+  P.iscalars = in->discal;
+  P.trace = nullptr;
+  if (in->trace_host) {
+    TraceEv* dptr = nullptr;
+    int* cptr = nullptr;
+    cudaHostGetDevicePointer(&dptr, in->trace_host, 0);
+    cudaHostGetDevicePointer(&cptr, in->trace_count_host, 0);
+    P.trace = dptr;
+    P.trace_count = cptr;
+    P.trace_cap = in->trace_cap;
+  }
+  return P;
+}
+
+// Launch the persistent kernel; returns the solver status and fills *so.
+int launch(cuhallar_instance* in, Params& P, int grid, cudaStream_t st, SolveOut* so,
+           float* ms = nullptr) {
+  ck(cudaMemsetAsync(in->bar, 0, sizeof(unsigned long long), st), "memset bar");
+  ck(cudaMemsetAsync(in->dso, 0, sizeof(SolveOut), st), "memset out");
+  if (in->trace_count_host) *in->trace_count_host = 0;
+  SolveOut* dso = in->dso;
+  void* args[] = {&P, &dso};
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (ms) {
+    ck(cudaEventCreate(&e0), "event");
+    ck(cudaEventCreate(&e1), "event");
+    ck(cudaEventRecord(e0, st), "event");
+  }
+  ck(cudaLaunchCooperativeKernel((void*)hallar_kernel, dim3(grid), dim3(kThreads), args,
+                                 kSmemBytes, st),
+     "cooperative launch");
+  if (ms) ck(cudaEventRecord(e1, st), "event");
+  ck(cudaMemcpyAsync(so, in->dso, sizeof(SolveOut), cudaMemcpyDeviceToHost, st), "D2H out");
+  ck(cudaStreamSynchronize(st), "hallar_kernel");
+  if (ms) {
+    cudaEventElapsedTime(ms, e0, e1);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+  }
+  return so->status;
+}
+
+int status_to_rc(int st, int msg) {
+  if (st == kOk) return 0;
+  g_err = msg_text(msg);
+  if (st == kErrNumerical) return CUHALLAR_ERR_NUMERICAL;
+  if (st == kErrInput) return CUHALLAR_ERR_INPUT;
+  return CUHALLAR_ERR_CUDA;
+}
+
+template <class F>
+int guard(F&& f) {
+  try {
+    return f();
+  } catch (const hh::InputError& e) {
+    g_err = e.what();
+    return CUHALLAR_ERR_INPUT;
+  } catch (const std::ios_base::failure& e) {
+    g_err = e.what();
+    return CUHALLAR_ERR_IO;
+  } catch (const CudaError& e) {
+    g_err = e.what();
+    return CUHALLAR_ERR_CUDA;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return CUHALLAR_ERR_CUDA;
+  }
+}
+
+cuhallar_instance* finish_pairs(hh::HostInst&& h) {
+  auto in = std::make_unique<cuhallar_instance>();
+  in->h = std::move(h);
+  upload_pairs(in.get());
+  return in.release();
+}
+
+void check_pairs(const cuhallar_instance* in) {
+  if (in->h.family == kPhaseret)
+    throw hh::InputError("phase retrieval: device operator path not available in this build");
+}
+
+// column-major (host or device) U -> buffer 0 (row-major)
+void load_factor_dev(cuhallar_instance* in, const double* U_dev, int64_t ld, int s,
+                     cudaStream_t st) {
+  const int64_t n = in->h.n;
+  const int64_t tot = n * s;
+  to_rowmajor<<<unsigned((tot + 255) / 256), 256, 0, st>>>(U_dev, ld, s, n, in->buf[0]);
+  ck(cudaGetLastError(), "to_rowmajor");
+}
+void store_factor_dev(cuhallar_instance* in, const double* src_rowmajor, int s, double* dst,
+                      int64_t ld, cudaStream_t st) {
+  const int64_t n = in->h.n;
+  const int64_t tot = n * s;
+  to_colmajor<<<unsigned((tot + 255) / 256), 256, 0, st>>>(src_rowmajor, s, n, dst, ld);
+  ck(cudaGetLastError(), "to_colmajor");
+}
+// multiplier (length m, device) -> p_up / p_lo (+ trace scalar)
+double load_multiplier_dev(cuhallar_instance* in, const double* p_dev, double* up, double* lo,
+                           cudaStream_t st) {
+  const int64_t np = in->h.np;
+  ck(cudaMemcpyAsync(up, p_dev, sizeof(double) * np, cudaMemcpyDeviceToDevice, st), "D2D p");
+  gather_lower<<<unsigned((np + 255) / 256), 256, 0, st>>>(p_dev, in->lo_eid, np, lo);
+  ck(cudaGetLastError(), "gather_lower");
+  double pt = 0.0;
+  if (in->h.has_trace)
+    ck(cudaMemcpyAsync(&pt, p_dev + np, sizeof(double), cudaMemcpyDeviceToHost, st), "D2H pt");
+  ck(cudaStreamSynchronize(st), "multiplier");
+  return pt;
+}
+
+}  // namespace
+
+// ==================================================================== ABI ===
+extern "C" {
+
+const char* cuhallar_last_error(void) { return g_err.c_str(); }
+const char* cuhallar_version(void) { return "cuhallar-b200 0.1.0 (sm_100a)"; }
+
+void cuhallar_config_default(cuhallar_config* c) {
+  std::memset(c, 0, sizeof(*c));
+  c->eps = 1e-5;
+  c->beta_growth = 2.0;
+  c->eps_decay = 0.5;
+  c->max_outer = 500;
+  c->time_limit = 3600.0;
+  c->seed = 0;
+  c->eig_tol = 1e-8;
+  c->eig_max_iters = 5000;
+  c->eig_block_restart = 30;
+  c->aipp_lambda0 = 10.0;
+  c->aipp_rho = 1e-4;
+  c->aipp_max_outer = 2000;
+  c->aipp_lambda_underflow = 1e-12;
+  c->fista_sigma = 0.3;
+  c->fista_chi = 0.5;
+  c->fista_mu = 0.5;
+  c->fista_L0 = 1.0;
+  c->fista_max_iters = 0;
+  c->max_fw_steps = 500;
+}
+
+int cuhallar_theta_hypercube(int d, cuhallar_instance** out) {
+  return guard([&] {
+    *out = finish_pairs(hh::make_theta(int64_t(1) << d, hh::edges_hypercube(d)));
+    return 0;
+  });
+}
+int cuhallar_theta_cycle(int n, cuhallar_instance** out) {
+  return guard([&] {
+    *out = finish_pairs(hh::make_theta(n, hh::edges_cycle(n)));
+    return 0;
+  });
+}
+int cuhallar_theta_petersen(cuhallar_instance** out) {
+  return guard([&] {
+    *out = finish_pairs(hh::make_theta(10, hh::edges_petersen()));
+    return 0;
+  });
+}
+int cuhallar_theta_edges(int64_t n_vertices, int64_t n_pairs, const int64_t* u, const int64_t* v,
+                         cuhallar_instance** out) {
+  return guard([&] {
+    hh::Edges raw(static_cast<size_t>(n_pairs));
+    for (int64_t k = 0; k < n_pairs; ++k) raw[k] = {u[k], v[k]};
+    int64_t n = 0;
+    const auto e = hh::normalise_edges(n_vertices, raw, &n);
+    *out = finish_pairs(hh::make_theta(n, e));
+    return 0;
+  });
+}
+int cuhallar_theta_file(const char* path, int fmt, cuhallar_instance** out) {
+  return guard([&] {
+    int64_t n = 0;
+    const auto e = hh::edges_from_file(path, fmt, &n);
+    *out = finish_pairs(hh::make_theta(n, e));
+    return 0;
+  });
+}
+int cuhallar_gen_matrix_completion(int64_t n1, int64_t n2, int r, uint64_t seed, int offset,
+                                   double tau_safety, cuhallar_instance** out) {
+  return guard([&] {
+    *out = finish_pairs(hh::make_matcomp(n1, n2, r, seed, offset != 0, tau_safety));
+    return 0;
+  });
+}
+int64_t cuhallar_matcomp_constraint_count(int64_t n1, int64_t n2, int r, int offset) {
+  return hh::matcomp_count(n1, n2, r, offset != 0);
+}
+int cuhallar_gen_phase_retrieval(int64_t n, int L, uint64_t seed, double tau_slack,
+                                 cuhallar_instance** out) {
+  return guard([&] {
+    (void)hh::make_phaseret(n, L, seed, tau_slack);
+    throw hh::InputError("phase retrieval: device operator path not available in this build");
+    *out = nullptr;
+    return 0;
+  });
+}
+void cuhallar_instance_destroy(cuhallar_instance* inst) { delete inst; }
+
+int cuhallar_instance_get_info(const cuhallar_instance* in, cuhallar_instance_info* o) {
+  o->n = in->h.n;
+  o->m = in->h.m;
+  o->identity_constraint = in->h.has_trace ? in->h.m - 1 : -1;
+  o->field_kind = in->h.family == kPhaseret ? CUHALLAR_FIELD_COMPLEX_EMBEDDED : CUHALLAR_FIELD_REAL;
+  o->family = in->h.family;
+  o->tau = in->h.tau;
+  o->norm_b1 = in->h.norm_b1;
+  o->norm_C1 = in->h.norm_C1;
+  o->nuclear_norm = in->h.nuclear;
+  o->device_bytes = in->bytes;
+  return 0;
+}
+int cuhallar_instance_get_b(const cuhallar_instance* in, double* b) {
+  std::memcpy(b, in->h.b.data(), sizeof(double) * in->h.b.size());
+  return 0;
+}
+int cuhallar_instance_get_pairs(const cuhallar_instance* in, int64_t* i, int64_t* j) {
+  std::memcpy(i, in->h.pub_i.data(), sizeof(int64_t) * in->h.pub_i.size());
+  std::memcpy(j, in->h.pub_j.data(), sizeof(int64_t) * in->h.pub_j.size());
+  return 0;
+}
+int cuhallar_instance_get_phaseret(const cuhallar_instance* in, double* x, double* masks) {
+  if (x) std::memcpy(x, in->h.hidden_x.data(), sizeof(double) * 2 * in->h.hidden_x.size());
+  if (masks) std::memcpy(masks, in->h.masks.data(), sizeof(double) * 2 * in->h.masks.size());
+  return 0;
+}
+
+// --------------------------------------------------------------- operators ---
+static int run_op(cuhallar_instance* in, int op, const double* U_dev, int64_t ldu, int s,
+                  const double* vec_dev, double beta, double* out_vec, double* out_mat,
+                  int64_t ldo, double* val_host, cudaStream_t st) {
+  return guard([&] {
+    check_pairs(in);
+    if (s < 1 || s > kSMax) throw hh::InputError("factor rank must be in [1, 32]");
+    if (ldu < in->h.n) throw hh::InputError("leading dimension < n");
+    std::lock_guard<std::mutex> lk(in->mu);
+    const int grid = grid_size(0);
+    ensure_workspace(in, grid, 0, 30);
+    Params P = base_params(in, nullptr);
+    P.op = op;
+    P.s_in = s;
+    P.beta_in = beta;
+    load_factor_dev(in, U_dev, ldu, s, st);
+    if (op == kOpCPlusAdj || op == kOpAdj) {
+      P.q_trace_in = load_multiplier_dev(in, vec_dev, in->q_up, in->q_lo, st);
+    } else if (op == kOpAlValue || op == kOpAlValGrad || op == kOpAlGrad) {
+      P.p_trace = load_multiplier_dev(in, vec_dev, in->p_up, in->p_lo, st);
+    }
+    if (op == kOpMap) P.out_vec = out_vec;
+    double* rm = nullptr;
+    if (out_mat) {
+      rm = in->buf[11];
+      P.out_mat = rm;
+    }
+    SolveOut so{};
+    const int stt = launch(in, P, grid, st, &so);
+    if (stt != kOk) return status_to_rc(stt, so.msg);
+    if (out_mat) {
+      store_factor_dev(in, rm, s, out_mat, ldo, st);
+      ck(cudaStreamSynchronize(st), "store");
+    }
+    if (val_host) ck(cudaMemcpy(val_host, in->dscal, sizeof(double), cudaMemcpyDeviceToHost), "val");
+    return 0;
+  });
+}
+
+int cuhallar_apply_map(cuhallar_instance* in, const double* U, int64_t ldu, int s, double* out,
+                       cuhallar_stream st) {
+  return run_op(in, kOpMap, U, ldu, s, nullptr, 0.0, out, nullptr, 0, nullptr, (cudaStream_t)st);
+}
+int cuhallar_apply_C(cuhallar_instance* in, const double* U, int64_t ldu, int s, double* out,
+                     int64_t ldo, cuhallar_stream st) {
+  return run_op(in, kOpApplyC, U, ldu, s, nullptr, 0.0, nullptr, out, ldo, nullptr,
+                (cudaStream_t)st);
+}
+int cuhallar_apply_adjoint(cuhallar_instance* in, const double* p, const double* U, int64_t ldu,
+                           int s, double* out, int64_t ldo, cuhallar_stream st) {
+  return run_op(in, kOpAdj, U, ldu, s, p, 0.0, nullptr, out, ldo, nullptr, (cudaStream_t)st);
+}
+int cuhallar_c_plus_adjoint(cuhallar_instance* in, const double* q, const double* U, int64_t ldu,
+                            int s, double* out, int64_t ldo, cuhallar_stream st) {
+  return run_op(in, kOpCPlusAdj, U, ldu, s, q, 0.0, nullptr, out, ldo, nullptr, (cudaStream_t)st);
+}
+int cuhallar_al_value(cuhallar_instance* in, const double* U, int64_t ldu, int s, const double* p,
+                      double beta, double* val, cuhallar_stream st) {
+  if (!(beta > 0)) {
+    g_err = "al_value: beta must be positive";
+    return CUHALLAR_ERR_INPUT;
+  }
+  return run_op(in, kOpAlValue, U, ldu, s, p, beta, nullptr, nullptr, 0, val, (cudaStream_t)st);
+}
+int cuhallar_al_gradient(cuhallar_instance* in, const double* U, int64_t ldu, int s,
+                         const double* p, double beta, double* grad, int64_t ldg,
+                         cuhallar_stream st) {
+  if (!(beta > 0)) {
+    g_err = "al_gradient: beta must be positive";
+    return CUHALLAR_ERR_INPUT;
+  }
+  return run_op(in, kOpAlGrad, U, ldu, s, p, beta, nullptr, grad, ldg, nullptr, (cudaStream_t)st);
+}
+int cuhallar_al_value_and_gradient(cuhallar_instance* in, const double* U, int64_t ldu, int s,
+                                   const double* p, double beta, double* val, double* grad,
+                                   int64_t ldg, cuhallar_stream st) {
+  return run_op(in, kOpAlValGrad, U, ldu, s, p, beta, nullptr, grad, ldg, val, (cudaStream_t)st);
+}
+
+// ------------------------------------------------------------------ solve ---
+static void host_factor_to_buf0(cuhallar_instance* in, const double* U_host, int s) {
+  const int64_t n = in->h.n;
+  std::vector<double> rm(size_t(n) * s);
+  for (int64_t a = 0; a < n; ++a)
+    for (int k = 0; k < s; ++k) rm[a * s + k] = U_host[a + k * n];
+  ck(cudaMemcpy(in->buf[0], rm.data(), rm.size() * sizeof(double), cudaMemcpyHostToDevice), "U0");
+}
+static double host_multiplier_to_dev(cuhallar_instance* in, const double* p_host) {
+  const int64_t np = in->h.np;
+  std::vector<double> up(np), lo(np);
+  for (int64_t k = 0; k < np; ++k) up[k] = p_host ? p_host[k] : 0.0;
+  for (int64_t e = 0; e < np; ++e) lo[e] = up[in->lo_eid_host[e]];
+  ck(cudaMemcpy(in->p_up, up.data(), np * sizeof(double), cudaMemcpyHostToDevice), "p_up");
+  ck(cudaMemcpy(in->p_lo, lo.data(), np * sizeof(double), cudaMemcpyHostToDevice), "p_lo");
+  return (in->h.has_trace && p_host) ? p_host[np] : 0.0;
+}
+
+int cuhallar_solve(cuhallar_instance* in, const cuhallar_config* cfg, const double* U0_host,
+                   int s0, const double* p0_host, cuhallar_report* rep, cuhallar_solution** sol,
+                   cuhallar_trace_fn fn, void* user) {
+  return guard([&] {
+    check_pairs(in);
+    validate_cfg(*cfg);
+    std::lock_guard<std::mutex> lk(in->mu);
+    const auto t_start = std::chrono::steady_clock::now();
+    const int64_t n = in->h.n;
+    const int grid = grid_size(cfg->team_ctas);
+    ensure_workspace(in, grid, cfg->seed, cfg->eig_block_restart);
+    int s = 1;
+    if (U0_host) {
+      if (s0 < 1 || s0 > kSMax) throw hh::InputError("solve: warm-start rank must be in [1, 32]");
+      double nrm = 0.0;
+      std::vector<double> tmp(U0_host, U0_host + n * s0);
+      nrm = std::sqrt(hh::eigen_order_sum_sq(tmp.data(), n * s0));
+      if (!(nrm <= 1.0 + 1e-12)) throw hh::InputError("solve: warm-start factor outside unit ball");
+      s = s0;
+      host_factor_to_buf0(in, U0_host, s);
+    } else {
+      // u0 = gaussian_vector(n, Rng(seed)); U0 = u0/|u0|  (solver.cpp:130-132)
+      std::vector<double> u0 = hh::gaussian_stream(cfg->seed, n);
+      const double nu = std::sqrt(hh::eigen_order_sum_sq(u0.data(), n));
+      for (auto& x : u0) x = x / nu;
+      ck(cudaMemcpy(in->buf[0], u0.data(), n * sizeof(double), cudaMemcpyHostToDevice), "U0");
+    }
+    Params P = base_params(in, cfg);
+    P.op = kOpSolve;
+    P.s_in = s;
+    P.p_trace = host_multiplier_to_dev(in, p0_host);
+    SolveOut so{};
+    float ms = 0.f;
+    const int stt = launch(in, P, grid, 0, &so, &ms);
+    const double wall =
+        std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();
+    if (fn && cfg->trace) {
+      const int cnt = std::min(*in->trace_count_host, in->trace_cap);
+      for (int i = 0; i < cnt; ++i) {
+        const TraceEv& e = in->trace_host[i];
+        cuhallar_trace_event ev{e.kind, e.outer_iter, e.beta, e.eps_inner, e.gap, e.theta,
+                                e.rank, e.al_value, e.fw_alpha, e.rel_pfeas, e.rel_gap,
+                                e.rel_dfeas};
+        fn(&ev, user);
+      }
+    }
+    if (stt != 0 && stt != 1 && stt != 2 && stt != 3) return status_to_rc(stt, so.msg);
+    if (so.status == kErrInput || so.status == kErrCapacity) return status_to_rc(so.status, so.msg);
+    const double tau = in->h.tau;
+    std::memset(rep, 0, sizeof(*rep));
+    rep->status = so.status;
+    rep->pval = tau * so.pval;
+    rep->dval = tau * so.dval;
+    rep->dval_no_theta = tau * so.dval_no_theta;
+    rep->rel_pfeas = so.rel_pfeas;
+    rep->rel_gap = so.rel_gap;
+    rep->rel_dfeas = so.rel_dfeas;
+    rep->rank = so.rank;
+    rep->outer_iters = so.outer_iters;
+    rep->fw_steps = so.fw_steps;
+    rep->aipp_iters = so.aipp_iters;
+    rep->fista_iters = so.fista_iters;
+    rep->eig_products = so.eig_products;
+    rep->wall_seconds = wall;
+    rep->device_seconds = ms * 1e-3;
+    rep->tau = tau;
+    rep->theta = so.theta;
+    rep->trace_dropped = std::max(0, *in->trace_count_host - in->trace_cap);
+    std::snprintf(rep->message, sizeof(rep->message), "%s", msg_text(so.msg));
+    if (sol) {
+      auto S = std::make_unique<cuhallar_solution>();
+      S->n = n;
+      S->m = in->h.m;
+      S->rank = so.rank;
+      std::vector<double> rm(size_t(n) * so.rank);
+      ck(cudaMemcpy(rm.data(), in->buf[so.out_buf], rm.size() * sizeof(double),
+                    cudaMemcpyDeviceToHost),
+         "U out");
+      S->U.resize(rm.size());
+      for (int64_t a = 0; a < n; ++a)
+        for (int k = 0; k < so.rank; ++k) S->U[a + k * n] = rm[a * so.rank + k];
+      S->p.resize(in->h.m);
+      ck(cudaMemcpy(S->p.data(), in->p_up, in->h.np * sizeof(double), cudaMemcpyDeviceToHost),
+         "p out");
+      if (in->h.has_trace) S->p[in->h.np] = so.p_trace;
+      *sol = S.release();
+    }
+    return 0;
+  });
+}
+
+int cuhallar_solution_get_U(const cuhallar_solution* s, double* U) {
+  std::memcpy(U, s->U.data(), s->U.size() * sizeof(double));
+  return 0;
+}
+int cuhallar_solution_get_p(const cuhallar_solution* s, double* p) {
+  std::memcpy(p, s->p.data(), s->p.size() * sizeof(double));
+  return 0;
+}
+void cuhallar_solution_destroy(cuhallar_solution* s) { delete s; }
+
+int cuhallar_min_eig_gradient(cuhallar_instance* in, const double* U_host, int s,
+                              const double* p_host, double beta, double tol, int max_iters,
+                              int block_restart, uint64_t seed, double* lambda, double* v_host,
+                              double* residual, int* matvecs, int* converged) {
+  return guard([&] {
+    check_pairs(in);
+    if (s < 1 || s > kSMax) throw hh::InputError("factor rank must be in [1, 32]");
+    if (block_restart < 2 || block_restart > kLanczosMax)
+      throw hh::InputError("eig: block_restart must lie in [2, 32]");
+    std::lock_guard<std::mutex> lk(in->mu);
+    const int grid = grid_size(0);
+    ensure_workspace(in, grid, seed, block_restart);
+    cuhallar_config cfg;
+    cuhallar_config_default(&cfg);
+    cfg.eig_max_iters = max_iters;
+    cfg.eig_block_restart = block_restart;
+    Params P = base_params(in, &cfg);
+    P.op = kOpMinEigG;
+    P.s_in = s;
+    P.beta_in = beta;
+    P.rho_in = tol;
+    host_factor_to_buf0(in, U_host, s);
+    P.p_trace = host_multiplier_to_dev(in, p_host);
+    double* vout = in->buf[11];
+    P.out_vec = vout;
+    SolveOut so{};
+    const int stt = launch(in, P, grid, 0, &so);
+    if (stt != kOk) return status_to_rc(stt, so.msg);
+    double sc[2];
+    int isc[2];
+    ck(cudaMemcpy(sc, in->dscal, sizeof(sc), cudaMemcpyDeviceToHost), "scalars");
+    ck(cudaMemcpy(isc, in->discal, sizeof(isc), cudaMemcpyDeviceToHost), "iscalars");
+    *lambda = sc[0];
+    *residual = sc[1];
+    *matvecs = isc[0];
+    *converged = isc[1];
+    if (v_host) ck(cudaMemcpy(v_host, vout, in->h.n * sizeof(double), cudaMemcpyDeviceToHost), "v");
+    return 0;
+  });
+}
+
+int cuhallar_aipp(cuhallar_instance* in, const double* p_host, double beta, const double* W_host,
+                  int s, double rho, const cuhallar_config* cfg, double* W_out, int* status,
+                  int* prox_iters, int* fista_iters, double* R_norm, double* g_value,
+                  double* lambda) {
+  return guard([&] {
+    check_pairs(in);
+    if (s < 1 || s > kSMax) throw hh::InputError("factor rank must be in [1, 32]");
+    std::lock_guard<std::mutex> lk(in->mu);
+    const int grid = grid_size(cfg ? cfg->team_ctas : 0);
+    ensure_workspace(in, grid, 0, 30);
+    Params P = base_params(in, cfg);
+    P.op = kOpAipp;
+    P.s_in = s;
+    P.beta_in = beta;
+    P.rho_in = rho;
+    host_factor_to_buf0(in, W_host, s);
+    P.p_trace = host_multiplier_to_dev(in, p_host);
+    double* wout = in->buf[11];
+    P.out_mat = wout;
+    SolveOut so{};
+    const int stt = launch(in, P, grid, 0, &so);
+    if (stt != kOk) return status_to_rc(stt, so.msg);
+    double sc[3];
+    int isc[3];
+    ck(cudaMemcpy(sc, in->dscal, sizeof(sc), cudaMemcpyDeviceToHost), "scalars");
+    ck(cudaMemcpy(isc, in->discal, sizeof(isc), cudaMemcpyDeviceToHost), "iscalars");
+    *R_norm = sc[0];
+    *g_value = sc[1];
+    *lambda = sc[2];
+    *status = isc[0];
+    *prox_iters = isc[1];
+    *fista_iters = isc[2];
+    std::vector<double> rm(size_t(in->h.n) * s);
+    ck(cudaMemcpy(rm.data(), wout, rm.size() * sizeof(double), cudaMemcpyDeviceToHost), "W");
+    for (int64_t a = 0; a < in->h.n; ++a)
+      for (int k = 0; k < s; ++k) W_out[a + k * in->h.n] = rm[a * s + k];
+    return 0;
+  });
+}
+
+}  // extern "C"

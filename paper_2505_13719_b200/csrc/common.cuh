@@ -1,0 +1,139 @@
+// Shared host/device definitions for the B200 HALLaR solver.
+#pragma once
+
+#include <cstdint>
+
+namespace hallar {
+
+constexpr int kThreads = 512;            // threads per persistent CTA
+constexpr int kWarps = kThreads / 32;
+constexpr int kSMax = 32;                // max factor rank (one lane per column)
+constexpr int kLanczosMax = 32;          // max Lanczos basis (block_restart cap)
+constexpr int kRedK = 40;                // max values per team reduction
+constexpr int kNBuf = 12;                // n x kSMax factor buffers in the pool
+constexpr int kTile = 8;                 // columns per fold chunk
+
+enum Family : int { kTheta = 0, kMatcomp = 1, kPhaseret = 2 };
+
+enum Status : int {
+  kOk = 0,
+  kErrInput = 64,
+  kErrNumerical = 3,
+  kErrCapacity = 65,  // rank or Lanczos refill capacity exceeded
+};
+
+// Pair-constraint instance as resident in HBM (theta / graph / matcomp).
+// Constraints k < np are X_{ei[k], ej[k]} with ei < ej, sorted by (ei, ej);
+// theta adds the trace constraint k = np (= m-1).  Rows are vertices.
+//   upper CSR: row a owns edges k in [up_ptr[a], up_ptr[a+1]) (ei[k] == a)
+//   lower CSR: row a owns lo entries e in [lo_ptr[a], lo_ptr[a+1]) with
+//              lo_col[e] = ei[k], lo_eid[e] = k, ej[k] == a, sorted by k.
+// Every lower k of row a precedes every upper k of row a, so folding lower
+// then upper entries reproduces the reference's increasing-k accumulation
+// order (instances.cpp:45-52).
+struct DevPairs {
+  int family = kTheta;
+  int has_trace = 0;
+  int64_t n = 0, np = 0, m = 0;
+  const int32_t* ei = nullptr;
+  const int32_t* ej = nullptr;
+  const int64_t* up_ptr = nullptr;
+  const int64_t* lo_ptr = nullptr;
+  const int32_t* lo_col = nullptr;
+  const int64_t* lo_eid = nullptr;
+  const double* b_up = nullptr;  // scaled b (edge order), null = all zero
+  const double* b_lo = nullptr;  // scaled b (lower order)
+  double b_trace = 0.0;          // scaled b[m-1] (theta)
+  double norm_b1 = 0.0, nb2 = 0.0, norm_C1 = 0.0;  // scaled instance norms
+};
+
+// Solver configuration (mirrors cuhallar_config / SolverConfig).
+struct Cfg {
+  double eps, beta0, beta_growth, eps0, eps_decay, eps_floor;
+  int max_outer;
+  double time_limit;
+  double eig_tol;
+  int eig_max_iters, eig_block_restart;
+  double aipp_lambda0, aipp_rho;
+  int aipp_max_outer;
+  double aipp_lambda_underflow;
+  double fista_sigma, fista_chi, fista_mu, fista_L0;
+  int fista_max_iters, max_fw_steps;
+  int trace;
+};
+
+struct TraceEv {
+  int kind, outer_iter;
+  double beta, eps_inner, gap, theta;
+  int64_t rank;
+  double al_value, fw_alpha, rel_pfeas, rel_gap, rel_dfeas;
+};
+
+// Operation selector for the persistent kernel.
+enum Op : int {
+  kOpSolve = 0,
+  kOpMap = 1,          // out_vec = A(UU') (edge order, trace at m-1)
+  kOpCPlusAdj = 2,     // out = CU + (A* q)U, q given (edge + lower order)
+  kOpAdj = 3,          // out = (A* q)U
+  kOpApplyC = 4,       // out = CU
+  kOpAlValue = 5,      // scalars[0] = L_beta(UU'; p)
+  kOpAlValGrad = 6,    // scalars[0] = value, out = gradient
+  kOpAlGrad = 7,       // out = gradient
+  kOpMinEigG = 8,      // Lanczos on G(U,p,beta)
+  kOpAipp = 9,         // aipp on L_beta(.;p) from U
+};
+
+// Everything the persistent kernel touches; lives in device memory.
+struct Params {
+  int op = kOpSolve;
+  DevPairs I;
+  Cfg cfg;
+  // team
+  unsigned long long* bar = nullptr;
+  double* slots = nullptr;  // [2][G][kRedK]
+  // factor pool, row-major n x s (stride s) inside capacity n x kSMax
+  double* buf[kNBuf] = {};
+  // Lanczos column slots (n each), plus w
+  double* vslot = nullptr;
+  int nslot = 0;
+  double* lw = nullptr;
+  const double* lz_rand = nullptr;  // n * (1 + n_refill) host-generated N(0,1)
+  int n_refill = 0;
+  // multipliers / gradient operator (edge + lower order)
+  double* p_up = nullptr;
+  double* p_lo = nullptr;
+  double* q_up = nullptr;
+  double* q_lo = nullptr;
+  double* r_up = nullptr;
+  double* r_lo = nullptr;
+  double p_trace = 0.0;      // p[m-1] input (theta)
+  // op inputs
+  int s_in = 1;              // rank of buf[0] input
+  double beta_in = 0.0;
+  double q_trace_in = 0.0;   // kOpCPlusAdj / kOpAdj: q[m-1]
+  double rho_in = 0.0;
+  double* out_vec = nullptr; // kOpMap
+  double* out_mat = nullptr; // row-major n x s
+  // outputs
+  double* scalars = nullptr; // device scalars out
+  int* iscalars = nullptr;
+  // trace ring (host mapped)
+  TraceEv* trace = nullptr;
+  int trace_cap = 0;
+  int* trace_count = nullptr;
+  // start vector (solve): buf[0] holds U0 (s_in columns)
+};
+
+// Solve outputs written by CTA 0 (device memory, copied back by the host).
+struct SolveOut {
+  int status;
+  int outer_iters, fw_steps;
+  int out_buf;     // index of the buffer holding the final U
+  int rank;
+  long long aipp_iters, fista_iters, eig_products;
+  double pval, dval, dval_no_theta, rel_pfeas, rel_gap, rel_dfeas;
+  double theta, p_trace;
+  int msg;         // message id
+};
+
+}  // namespace hallar

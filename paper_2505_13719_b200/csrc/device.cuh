@@ -1,0 +1,698 @@
+// Device-resident HALLaR for pair-constraint instances (Lovasz theta on any
+// graph, matrix completion).  The whole solve — outer AL loop, HLR, ADAP-AIPP,
+// ADAP-FISTA, thick-restart Lanczos, certificate — runs inside ONE persistent
+// cooperative kernel; scalars are reduced deterministically and replicated in
+// every thread, so the control flow never leaves the GPU.
+//
+// Reference statements are cited as file:line into /root/reference/proj/src.
+// Arithmetic is compiled with -fmad=false so element-wise expressions round
+// exactly like the reference's SSE2 build (no FMA contraction).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+#include "team.cuh"
+
+namespace hallar {
+
+constexpr unsigned kFull = 0xffffffffu;
+constexpr int kTileLd = 33;  // padded fold tile stride (conflict-free)
+constexpr int kHLd = kLanczosMax + 1;
+
+enum Msg : int {
+  kMsgNone = 0,
+  kMsgFistaDiverged = 1,
+  kMsgAlValue = 2,
+  kMsgAlValGrad = 3,
+  kMsgAlGrad = 4,
+  kMsgGradOp = 5,
+  kMsgProjectBall = 6,
+  kMsgNonFinite = 7,
+  kMsgRankCap = 8,
+  kMsgRefillCap = 9,
+  kMsgRank32 = 10,
+};
+
+struct Ctx {
+  Team t;
+  RedSmem rs;
+  double* tile;   // this warp's fold tile [kTile][kTileLd]
+  double* cs;     // [kSMax] column sums of the gathered factor (theta C-term)
+  double* H;      // [kHLd][kHLd] Lanczos projected matrix (column-major)
+  double* JA;     // [32*32] Jacobi work
+  double* JV;     // [32*32]
+  double* E;      // [32*32] sorted eigenvectors
+  double* ev;     // [32] sorted eigenvalues
+  double* jcs;    // [32] rotation cos/sin pairs
+  int* jpq;       // [32] pair indices
+  double* vsum;   // [nslot] column sums of Lanczos slots (theta)
+  int* col;       // [kHLd+1] Lanczos basis -> slot
+  int64_t rl, rh;  // rows owned by this CTA (nnz-balanced)
+  int64_t kl, kh;  // edges owned by this CTA
+  double* hh;     // [32] Lanczos CGS coefficients
+  double* hh2;    // [32]
+  int warp, lane;
+  int status = kOk;
+  int msg = kMsgNone;
+  double beta = 0.0;     // current AL penalty (replicated)
+  double p_trace = 0.0;  // current p[m-1] (theta trace multiplier)
+};
+
+__device__ __forceinline__ bool is_theta(const DevPairs& I) { return I.has_trace != 0; }
+
+__device__ __forceinline__ void fail(Ctx& c, int status, int msg) {
+  if (c.status == kOk) {
+    c.status = status;
+    c.msg = msg;
+  }
+}
+
+// ------------------------------------------------------------------ layout --
+// Rows are split so that (lower + upper entries + 8) is balanced per CTA.
+__device__ int64_t work_prefix(const DevPairs& I, int64_t a) {
+  return I.lo_ptr[a] + I.up_ptr[a] + 8 * a;
+}
+__device__ int64_t row_split(const DevPairs& I, int rank, int size) {
+  if (rank <= 0) return 0;
+  if (rank >= size) return I.n;
+  const int64_t total = work_prefix(I, I.n);
+  const int64_t target = (int64_t)((__int128)total * rank / size);
+  int64_t lo = 0, hi = I.n;  // first a with prefix >= target
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (work_prefix(I, mid) < target) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
+// ------------------------------------------------------------- row pass ---
+// For every row a owned by this CTA compute, lane c < s,
+//   h(a,c) = init(a,c) (+)fold_k 0.5 q_k U(b_k,c)        (k increasing)
+// where q_k = P_k (FIXED) or q_k = P_k + beta (U_a.U_b - b_k) (!FIXED), the
+// reference's C_plus_adjoint / adjoint_into (instances.cpp:39-55, 99-110,
+// 222-232).  init = alpha*U(a,c) - cs[c] (cs may be null) or 0.
+// !FIXED also accumulates over upper entries (each constraint once):
+//   sums[0] += p r, sums[1] += r^2, sums[2] += q (r + b).
+// epi(a, h, u_own) is called warp-uniformly; lanes >= s carry junk.
+template <int S, bool FIXED, class Epi>
+__device__ __noinline__ void row_pass(Ctx& c, const Params& P, const double* __restrict__ U, int s_rt,
+                         const double* __restrict__ Pup, const double* __restrict__ Plo,
+                         double beta, double alpha, const double* cs, bool zero_init,
+                         double (&sums)[3], Epi& epi) {
+  const DevPairs& I = P.I;
+  constexpr int SR = S > 0 ? S : kSMax;
+  const int s = S > 0 ? S : s_rt;
+  const int lane = c.lane;
+  double* tile = c.tile;
+  for (int64_t a = c.rl + c.warp; a < c.rh; a += kWarps) {
+    double ua[SR];
+#pragma unroll
+    for (int k = 0; k < SR; ++k) ua[k] = (k < s) ? U[a * s + k] : 0.0;
+    const double uown = lane < s ? U[a * s + lane] : 0.0;
+    double acc = 0.0;
+    if (lane < s && !zero_init) {
+      acc = alpha * uown;
+      if (cs) acc = acc - cs[lane];
+    }
+    const int64_t lo0 = I.lo_ptr[a], nlo = I.lo_ptr[a + 1] - lo0;
+    const int64_t up0 = I.up_ptr[a], nup = I.up_ptr[a + 1] - up0;
+    const int64_t tot = nlo + nup;
+    for (int64_t base = 0; base < tot; base += 32) {
+      const int64_t e = base + lane;
+      const bool valid = e < tot;
+      const bool upper = e >= nlo;
+      int64_t b = 0;
+      double pq = 0.0, bb = 0.0;
+      if (valid) {
+        if (!upper) {
+          b = I.lo_col[lo0 + e];
+          pq = Plo[lo0 + e];
+          if (!FIXED && I.b_lo) bb = I.b_lo[lo0 + e];
+        } else {
+          const int64_t k = up0 + (e - nlo);
+          b = I.ej[k];
+          pq = Pup[k];
+          if (!FIXED && I.b_up) bb = I.b_up[k];
+        }
+      }
+      double ub[SR];
+#pragma unroll
+      for (int k = 0; k < SR; ++k) ub[k] = (valid && k < s) ? U[b * s + k] : 0.0;
+      double w = 0.0;
+      if (valid) {
+        if (FIXED) {
+          w = 0.5 * pq;
+        } else {
+          double d = ua[0] * ub[0];
+#pragma unroll
+          for (int k = 1; k < SR; ++k)
+            if (k < s) d = d + ua[k] * ub[k];
+          const double r = d - bb;
+          const double q = pq + beta * r;
+          w = 0.5 * q;
+          if (upper) {
+            sums[0] = sums[0] + pq * r;
+            sums[1] = sums[1] + r * r;
+            sums[2] = sums[2] + q * (r + bb);
+          }
+        }
+      }
+      const unsigned skip = __ballot_sync(kFull, !valid || w == 0.0);
+      const int cnt = (int)min((int64_t)32, tot - base);
+      for (int c0 = 0; c0 < s; c0 += kTile) {
+#pragma unroll
+        for (int t = 0; t < kTile; ++t) {
+          double ubt = 0.0;
+#pragma unroll
+          for (int k = 0; k < SR; ++k)
+            if (k == c0 + t) ubt = ub[k];
+          if (c0 + t < s) tile[t * kTileLd + lane] = w * ubt;
+        }
+        __syncwarp();
+        const int cl = lane - c0;
+        if (cl >= 0 && cl < kTile && lane < s) {
+          const double* tc = tile + cl * kTileLd;
+          for (int j = 0; j < cnt; ++j)
+            if (!((skip >> j) & 1u)) acc = acc + tc[j];
+        }
+        __syncwarp();
+      }
+    }
+    epi(a, acc, uown);
+  }
+}
+
+// GradientOperator build (sdp_instance.cpp:73-83): for every pair constraint
+// r_k = U_a.U_b - b_k and q_k = p_k + beta r_k, written in edge order (upper
+// entries) and lower order.  Upper entries accumulate p.r and r^2.
+template <int S>
+__device__ __noinline__ void gradop_pass(Ctx& c, const Params& P, const double* __restrict__ U, int s_rt,
+                            double beta, double (&sums)[2], bool* nonfinite) {
+  const DevPairs& I = P.I;
+  constexpr int SR = S > 0 ? S : kSMax;
+  const int s = S > 0 ? S : s_rt;
+  const int lane = c.lane;
+  bool bad = false;
+  for (int64_t a = c.rl + c.warp; a < c.rh; a += kWarps) {
+    double ua[SR];
+#pragma unroll
+    for (int k = 0; k < SR; ++k) ua[k] = (k < s) ? U[a * s + k] : 0.0;
+    const int64_t lo0 = I.lo_ptr[a], nlo = I.lo_ptr[a + 1] - lo0;
+    const int64_t up0 = I.up_ptr[a], nup = I.up_ptr[a + 1] - up0;
+    const int64_t tot = nlo + nup;
+    for (int64_t e = lane; e < tot; e += 32) {
+      const bool upper = e >= nlo;
+      int64_t b, idx;
+      double pq, bb = 0.0;
+      if (!upper) {
+        idx = lo0 + e;
+        b = I.lo_col[idx];
+        pq = P.p_lo[idx];
+        if (I.b_lo) bb = I.b_lo[idx];
+      } else {
+        idx = up0 + (e - nlo);
+        b = I.ej[idx];
+        pq = P.p_up[idx];
+        if (I.b_up) bb = I.b_up[idx];
+      }
+      double d = 0.0;
+#pragma unroll
+      for (int k = 0; k < SR; ++k)
+        if (k < s) {
+          const double t = ua[k] * U[b * s + k];
+          d = (k == 0) ? t : d + t;
+        }
+      const double r = d - bb;
+      const double q = pq + beta * r;
+      if (!isfinite(q)) bad = true;
+      if (!upper) {
+        P.r_lo[idx] = r;
+        P.q_lo[idx] = q;
+      } else {
+        P.r_up[idx] = r;
+        P.q_up[idx] = q;
+        sums[0] = sums[0] + pq * r;
+        sums[1] = sums[1] + r * r;
+      }
+    }
+  }
+  *nonfinite = bad;
+}
+
+// ------------------------------------------------------------- map pass ---
+// Thread per pair constraint k (edge order): d_k = U_{i_k}.U_{j_k} summed over
+// columns in order (instances.cpp:27-35).
+enum MapMode : int { kMapPR = 0, kMapRR = 1, kMapOut = 2, kMapFWS = 3 };
+template <int S>
+__device__ __noinline__ void map_pass(Ctx& c, const Params& P, const double* __restrict__ U, int s_rt,
+                         int mode, const double* __restrict__ pup, double* out,
+                         const double* __restrict__ ref, double (&sums)[2]) {
+  const DevPairs& I = P.I;
+  constexpr int SR = S > 0 ? S : kSMax;
+  const int s = S > 0 ? S : s_rt;
+  for (int64_t k = c.kl + threadIdx.x; k < c.kh; k += kThreads) {
+    const int64_t i = I.ei[k], j = I.ej[k];
+    double d = 0.0;
+#pragma unroll
+    for (int cc = 0; cc < SR; ++cc)
+      if (cc < s) {
+        const double t = U[i * s + cc] * U[j * s + cc];
+        d = (cc == 0) ? t : d + t;
+      }
+    const double bk = I.b_up ? I.b_up[k] : 0.0;
+    if (mode == kMapOut) {
+      out[k] = d;
+    } else if (mode == kMapFWS) {
+      const double t = (ref[k] + bk) - d;
+      sums[1] = sums[1] + t * t;
+    } else {
+      const double r = d - bk;
+      if (mode == kMapPR) sums[0] = sums[0] + pup[k] * r;
+      sums[1] = sums[1] + r * r;
+    }
+  }
+}
+
+// -------------------------------------------------------- factor helpers ---
+// Statistics of a factor needed before gathering it: theta needs ||U||_F^2
+// (trace constraint) and the column sums (C = -ee'); MC needs 0.5||U||^2.
+// On return (all CTAs): nrm2, and c.cs[0..s) filled for theta.
+template <int S>
+__device__ __noinline__ void factor_stats(Ctx& c, const Params& P, const double* __restrict__ U, int s_rt,
+                             double* nrm2) {
+  constexpr int SR = S > 0 ? S : kSMax;
+  const int s = S > 0 ? S : s_rt;
+  double v[SR + 1];
+#pragma unroll
+  for (int k = 0; k <= SR; ++k) v[k] = 0.0;
+  for (int64_t a = c.rl + threadIdx.x; a < c.rh; a += kThreads) {
+#pragma unroll
+    for (int k = 0; k < SR; ++k)
+      if (k < s) {
+        const double u = U[a * s + k];
+        v[0] = v[0] + u * u;
+        v[1 + k] = v[1 + k] + u;
+      }
+  }
+  team_sum<SR + 1>(c.t, c.rs, v);
+  *nrm2 = v[0];
+  if (threadIdx.x < (unsigned)s) c.cs[threadIdx.x] = c.rs.out[1 + threadIdx.x];
+  __syncthreads();
+}
+
+// <CU, U> from the statistics: theta -sum_c cs_c^2, MC 0.5||U||^2.
+__device__ __forceinline__ double cdot_from_stats(const Ctx& c, const DevPairs& I, int s,
+                                                  double nrm2) {
+  if (is_theta(I)) {
+    double t = 0.0;
+    for (int k = 0; k < s; ++k) t = t + c.cs[k] * c.cs[k];
+    return -t;
+  }
+  return 0.5 * nrm2;
+}
+
+__device__ __forceinline__ double theta_alpha_or_half(const DevPairs& I, double qt) {
+  return is_theta(I) ? qt : 0.5;
+}
+
+template <int S>
+__device__ __noinline__ void copy_rows(Ctx& c, const double* __restrict__ src, double* dst, int s_rt) {
+  const int s = S > 0 ? S : s_rt;
+  for (int64_t a = c.rl + threadIdx.x; a < c.rh; a += kThreads)
+    for (int k = 0; k < s; ++k) dst[a * s + k] = src[a * s + k];
+}
+
+// al_value (sdp_instance.cpp:50-60) at U: stats pass + map pass.
+// Leaves c.cs = colsum(U) (theta).
+template <int S>
+__device__ __noinline__ bool al_value_dev(Ctx& c, const Params& P, const double* U, int s, const double* pup,
+                             double p_trace, double beta, double* val, double* nrm2_out) {
+  const DevPairs& I = P.I;
+  double nrm2;
+  factor_stats<S>(c, P, U, s, &nrm2);
+  double sums[2] = {0.0, 0.0};
+  map_pass<S>(c, P, U, s, kMapPR, pup, nullptr, nullptr, sums);
+  team_sum<2>(c.t, c.rs, sums);
+  double pr = sums[0], rr = sums[1];
+  if (is_theta(I)) {
+    const double rt = nrm2 - I.b_trace;
+    pr = pr + p_trace * rt;
+    rr = rr + rt * rt;
+  }
+  const double cdot = cdot_from_stats(c, I, s, nrm2);
+  const double v = cdot + pr + 0.5 * beta * rr;
+  if (nrm2_out) *nrm2_out = nrm2;
+  if (!isfinite(v)) {
+    fail(c, kErrNumerical, kMsgAlValue);
+    return false;
+  }
+  *val = v;
+  return true;
+}
+
+// ------------------------------------------------------------ ADAP-FISTA ---
+struct Roles {
+  int rep, yt, wp, best, x, y, xt, gt, yn, v, tmp;
+};
+
+struct FistaOut {
+  int status;  // 0 success, 1 failure, 2 iter limit
+  double L, psi_y, dist0;
+  int iters;
+};
+
+// fista_run on psi(u) = lambda L_beta(uu';p) + 0.5||u - W||^2 from x0 = W
+// (adap_fista.cpp:14-103, adap_aipp.cpp:20-36).  On success buffers[yn]
+// holds y and buffers[v] holds v.
+template <int S>
+__device__ __noinline__ bool fista_dev(Ctx& c, const Params& P, Roles& R, int s, double lambda, double L0,
+                          FistaOut& out) {
+  const DevPairs& I = P.I;
+  const Cfg& cf = P.cfg;
+  constexpr int SR = S > 0 ? S : kSMax;
+  const double mu = cf.fista_mu, chi = cf.fista_chi, sigma = cf.fista_sigma;
+  const double beta = c.beta;
+  const double pt = c.p_trace;
+  double A = 0.0, tau = 1.0, L = L0;
+  // x = y = x0
+  {
+    const double* W = P.buf[R.wp];
+    double* X = P.buf[R.x];
+    double* Y = P.buf[R.y];
+    for (int64_t a = c.rl + threadIdx.x; a < c.rh; a += kThreads)
+      for (int k = 0; k < s; ++k) {
+        X[a * s + k] = W[a * s + k];
+        Y[a * s + k] = W[a * s + k];
+      }
+  }
+  for (int it = 0;; ++it) {
+    const int cap = cf.fista_max_iters > 0
+                        ? cf.fista_max_iters
+                        : 50 + (int)(10.0 * sqrt(L / mu) * log2(4.0 + L / L0));
+    if (it >= cap) {
+      out.status = 2;
+      out.L = L;
+      out.iters = it;
+      // y stays in R.y: callers treat it as failure
+      return true;
+    }
+    double a, psi_t, psi_n, dsq, dist0, nrmz, ny2;
+    for (;;) {
+      a = (tau + sqrt(tau * tau + 4.0 * tau * A * (L - mu))) / (2.0 * (L - mu));
+      // ---- T1: x_tilde = (A y + a x)/(A + a); ||xt - W||^2; theta stats
+      const double* W = P.buf[R.wp];
+      const double* X = P.buf[R.x];
+      const double* Y = P.buf[R.y];
+      double* XT = P.buf[R.xt];
+      double nt2 = 0.0, dd = 0.0;
+      {
+        double v[SR + 2];
+#pragma unroll
+        for (int k = 0; k < SR + 2; ++k) v[k] = 0.0;
+        for (int64_t r = c.rl + threadIdx.x; r < c.rh; r += kThreads) {
+#pragma unroll
+          for (int k = 0; k < SR; ++k)
+            if (k < s) {
+              const int64_t o = r * s + k;
+              const double xt = (A * Y[o] + a * X[o]) / (A + a);
+              XT[o] = xt;
+              const double dv = xt - W[o];
+              v[0] = v[0] + dv * dv;
+              v[1] = v[1] + xt * xt;
+              v[2 + k] = v[2 + k] + xt;
+            }
+        }
+        team_sum<SR + 2>(c.t, c.rs, v);
+        dd = v[0];
+        nt2 = v[1];
+        if (threadIdx.x < (unsigned)s) c.cs[threadIdx.x] = c.rs.out[2 + threadIdx.x];
+        __syncthreads();
+      }
+      // ---- T2: value_and_gradient at x_tilde fused with psi gradient and
+      //          the projection norm (sdp_instance.cpp:115-127)
+      double rt = 0.0, qt = 0.0;
+      if (is_theta(I)) {
+        rt = nt2 - I.b_trace;
+        qt = pt + beta * rt;
+      }
+      double* GT = P.buf[R.gt];
+      double hU = 0.0, zz = 0.0;
+      double sums[3] = {0.0, 0.0, 0.0};
+      {
+        auto epi = [&](int64_t row, double h, double xo) {
+          if (c.lane < s) {
+            const int64_t o = row * s + c.lane;
+            hU = hU + h * xo;
+            const double g = 2.0 * h;
+            const double gt = lambda * g + (xo - W[o]);
+            GT[o] = gt;
+            const double z = xo - gt / L;
+            zz = zz + z * z;
+          }
+        };
+        row_pass<S, false>(c, P, XT, s, P.p_up, P.p_lo, beta, theta_alpha_or_half(I, qt),
+                           is_theta(I) ? c.cs : nullptr, false, sums, epi);
+        double v[5] = {hU, sums[0], sums[1], sums[2], zz};
+        team_sum<5>(c.t, c.rs, v);
+        hU = v[0];
+        double pr = v[1], rr = v[2], qrb = v[3];
+        zz = v[4];
+        if (is_theta(I)) {
+          pr = pr + pt * rt;
+          rr = rr + rt * rt;
+          qrb = qrb + qt * (rt + I.b_trace);
+        }
+        const double cdot = hU - qrb;
+        const double val = cdot + pr + 0.5 * beta * rr;
+        if (!isfinite(val)) {
+          fail(c, kErrNumerical, kMsgAlValGrad);
+          return false;
+        }
+        psi_t = lambda * val + 0.5 * dd;
+      }
+      // ---- project_ball (sdp_instance.cpp:94-99)
+      if (!isfinite(zz)) {
+        fail(c, kErrInput, kMsgProjectBall);
+        return false;
+      }
+      nrmz = sqrt(zz);
+      const bool scale = !(nrmz <= 1.0);
+      // ---- T3: y_next; ||y-W||^2, ||y-xt||^2, <gt, y-xt>, stats of y
+      double* YN = P.buf[R.yn];
+      double v3[SR + 4];
+#pragma unroll
+      for (int k = 0; k < SR + 4; ++k) v3[k] = 0.0;
+      for (int64_t r = c.rl + threadIdx.x; r < c.rh; r += kThreads) {
+#pragma unroll
+        for (int k = 0; k < SR; ++k)
+          if (k < s) {
+            const int64_t o = r * s + k;
+            const double xt = XT[o], gt = GT[o];
+            const double z = xt - gt / L;
+            const double y = scale ? z / nrmz : z;
+            YN[o] = y;
+            const double d0 = y - W[o];
+            const double dx = y - xt;
+            v3[0] = v3[0] + d0 * d0;
+            v3[1] = v3[1] + dx * dx;
+            v3[2] = v3[2] + gt * dx;
+            v3[3] = v3[3] + y * y;
+            v3[4 + k] = v3[4 + k] + y;
+          }
+      }
+      c.t.sync();
+      // ---- T4: map at y_next (al_value, sdp_instance.cpp:50-60)
+      double ms[2] = {0.0, 0.0};
+      map_pass<S>(c, P, YN, s, kMapPR, P.p_up, nullptr, nullptr, ms);
+      {
+        double v[SR + 6];
+#pragma unroll
+        for (int k = 0; k < SR + 4; ++k) v[k] = v3[k];
+        v[SR + 4] = ms[0];
+        v[SR + 5] = ms[1];
+        team_sum<SR + 6>(c.t, c.rs, v);
+        dist0 = v[0];
+        dsq = v[1];
+        const double lin_s = v[2];
+        ny2 = v[3];
+        if (threadIdx.x < (unsigned)s) c.cs[threadIdx.x] = c.rs.out[4 + threadIdx.x];
+        __syncthreads();
+        double pr = v[SR + 4], rr = v[SR + 5];
+        if (is_theta(I)) {
+          const double r2 = ny2 - I.b_trace;
+          pr = pr + pt * r2;
+          rr = rr + r2 * r2;
+        }
+        const double cdot = cdot_from_stats(c, I, s, ny2);
+        const double val = cdot + pr + 0.5 * beta * rr;
+        if (!isfinite(val)) {
+          fail(c, kErrNumerical, kMsgAlValue);
+          return false;
+        }
+        psi_n = lambda * val + 0.5 * dist0;
+        const double lin = psi_t + lin_s;
+        const double noise = 1e-14 * (fabs(psi_n) + fabs(psi_t) + 1.0);
+        if (lin + (1.0 - chi) * L / 4.0 * dsq >= psi_n - noise) break;
+      }
+      L *= 2.0;
+      if (L > 1e18) {
+        fail(c, kErrNumerical, kMsgFistaDiverged);
+        return false;
+      }
+    }
+    const double A_next = A + a;
+    tau += a * mu;
+    if (dist0 < chi * A_next * L * dsq) {
+      out.status = 1;
+      out.L = L;
+      out.psi_y = psi_n;
+      out.iters = it + 1;
+      out.dist0 = dist0;
+      return true;
+    }
+    // ---- T5: gradient at y_next -> v; x update (adap_fista.cpp:68-71, 86-87)
+    {
+      const double* W = P.buf[R.wp];
+      const double* XT = P.buf[R.xt];
+      const double* GT = P.buf[R.gt];
+      const double* YN = P.buf[R.yn];
+      double* X = P.buf[R.x];
+      double* V = P.buf[R.v];
+      double qt = 0.0;
+      if (is_theta(I)) qt = pt + beta * (ny2 - I.b_trace);
+      double vv = 0.0;
+      const double Lm = L - mu, mua = mu * a, tam = tau - a * mu;
+      auto epi = [&](int64_t row, double h, double yo) {
+        if (c.lane < s) {
+          const int64_t o = row * s + c.lane;
+          const double g = 2.0 * h;
+          const double gy = lambda * g + (yo - W[o]);
+          const double xt = XT[o];
+          const double vt = gy - GT[o] + L * (xt - yo);
+          V[o] = vt;
+          vv = vv + vt * vt;
+          const double sd = Lm * (xt - yo);
+          X[o] = (mua * yo + tam * X[o] - a * sd) / tau;
+        }
+      };
+      double sums[3] = {0.0, 0.0, 0.0};
+      row_pass<S, false>(c, P, YN, s, P.p_up, P.p_lo, beta, theta_alpha_or_half(I, qt),
+                         is_theta(I) ? c.cs : nullptr, false, sums, epi);
+      double v[1] = {vv};
+      team_sum<1>(c.t, c.rs, v);
+      vv = v[0];
+      if (!isfinite(vv)) {
+        fail(c, kErrNumerical, kMsgAlGrad);
+        return false;
+      }
+      if (sqrt(vv) <= sigma * sqrt(dist0)) {
+        out.status = 0;
+        out.L = L;
+        out.psi_y = psi_n;
+        out.iters = it + 1;
+        out.dist0 = dist0;
+        return true;
+      }
+    }
+    A = A_next;
+    const int tmp = R.y;
+    R.y = R.yn;
+    R.yn = tmp;
+  }
+}
+
+// ------------------------------------------------------------- ADAP-AIPP ---
+struct AippOut {
+  int status;  // 0 converged, 1 iter limit, 2 lambda underflow
+  int w_buf;   // buffer holding the returned W
+  double R_norm, g_value, lambda;
+  int prox_iters, fista_iters;
+};
+
+// aipp_run (adap_aipp.cpp:40-116) from buffers[R.yt]; rho given.
+template <int S>
+__device__ __noinline__ bool aipp_dev(Ctx& c, const Params& P, Roles& R, int s, double rho, AippOut& out) {
+  const Cfg& cf = P.cfg;
+  double lambda = cf.aipp_lambda0, M_bar = 1.0;
+  // W_prev = W_init
+  copy_rows<S>(c, P.buf[R.yt], P.buf[R.wp], s);
+  __syncthreads();
+  double g_prev;
+  if (!al_value_dev<S>(c, P, P.buf[R.wp], s, P.p_up, c.p_trace, c.beta, &g_prev, nullptr))
+    return false;
+  out.w_buf = R.yt;  // out.W = W_init
+  out.R_norm = INFINITY;
+  out.g_value = g_prev;
+  out.lambda = lambda;
+  out.prox_iters = 0;
+  out.fista_iters = 0;
+  bool have_best = false;
+  for (int j = 1; j <= cf.aipp_max_outer; ++j) {
+    double L_out = 0.0, g_W = 0.0, Rn2 = 0.0;
+    for (;;) {
+      if (lambda < cf.aipp_lambda_underflow * cf.aipp_lambda0) {
+        out.status = 2;
+        if (have_best) out.w_buf = R.best;
+        return true;
+      }
+      FistaOut fo;
+      if (!fista_dev<S>(c, P, R, s, lambda, fmax(1.0, M_bar / 2.0), fo)) return false;
+      out.fista_iters += fo.iters;
+      if (fo.status == 0) {
+        const double step_sq = fo.dist0;
+        g_W = (fo.psi_y - 0.5 * step_sq) / lambda;
+        const double descent = lambda * g_prev - (lambda * g_W + 0.5 * step_sq);
+        // vw = <v, W_prev - y>, and ||(v + W_prev - y)/lambda||^2
+        const double* V = P.buf[R.v];
+        const double* Wp = P.buf[R.wp];
+        const double* Yn = P.buf[R.yn];
+        double v[2] = {0.0, 0.0};
+        for (int64_t a = c.rl + threadIdx.x; a < c.rh; a += kThreads)
+          for (int k = 0; k < s; ++k) {
+            const int64_t o = a * s + k;
+            const double vt = V[o], wp = Wp[o], y = Yn[o];
+            v[0] = v[0] + vt * (wp - y);
+            const double r = (vt + wp - y) / lambda;
+            v[1] = v[1] + r * r;
+          }
+        team_sum<2>(c.t, c.rs, v);
+        if (descent >= v[0]) {
+          L_out = fo.L;
+          Rn2 = v[1];
+          break;
+        }
+      }
+      lambda /= 2.0;
+    }
+    M_bar = L_out;
+    const double R_norm = sqrt(Rn2);
+    ++out.prox_iters;
+    if (R_norm <= rho) {
+      out.status = 0;
+      out.w_buf = R.yn;
+      out.R_norm = R_norm;
+      out.g_value = g_W;
+      out.lambda = lambda;
+      return true;
+    }
+    if (R_norm < out.R_norm) {
+      copy_rows<S>(c, P.buf[R.yn], P.buf[R.best], s);
+      have_best = true;
+      out.w_buf = R.best;
+      out.R_norm = R_norm;
+      out.g_value = g_W;
+      out.lambda = lambda;
+    }
+    // W_prev = W
+    const int tmp = R.wp;
+    R.wp = R.yn;
+    R.yn = tmp;
+    g_prev = g_W;
+    __syncthreads();
+  }
+  out.status = 1;
+  return true;
+}
+
+}  // namespace hallar

@@ -1,0 +1,411 @@
+// Outer augmented-Lagrangian driver + dual certificate (solver.cpp:51-279)
+// and the op dispatcher of the persistent kernel.
+#pragma once
+
+#include "solver.cuh"
+
+namespace hallar {
+
+struct Term {
+  double rel_pfeas, rel_gap, rel_dfeas, pval, dval, dual_lambda_min, bp_edges;
+  long long eig_products;
+  bool eig_trusted, done;
+};
+
+// check_termination (solver.cpp:51-76) with the multiplier (p_up, p_lo, pt).
+template <int S>
+__device__ __noinline__ bool check_termination_dev(Ctx& c, const Params& P, const double* U, int s, double pt,
+                                      double theta, double eig_tol, Term& t) {
+  const DevPairs& I = P.I;
+  const Cfg& cf = P.cfg;
+  double nrm2;
+  factor_stats<S>(c, P, U, s, &nrm2);
+  double ms[2] = {0.0, 0.0};
+  map_pass<S>(c, P, U, s, kMapRR, nullptr, nullptr, nullptr, ms);
+  double bp = 0.0;
+  if (I.b_up)
+    for (int64_t k = c.kl + threadIdx.x; k < c.kh; k += kThreads) bp = bp + I.b_up[k] * P.p_up[k];
+  double v[2] = {ms[1], bp};
+  team_sum<2>(c.t, c.rs, v);
+  double rr = v[0];
+  t.bp_edges = v[1];
+  double bpa = v[1];
+  if (is_theta(I)) {
+    const double r = nrm2 - I.b_trace;
+    rr = rr + r * r;
+    bpa = bpa + I.b_trace * pt;
+  }
+  t.rel_pfeas = sqrt(rr) / (1.0 + I.norm_b1);
+  t.pval = cdot_from_stats(c, I, s, nrm2);
+  t.dval = -bpa - theta;
+  t.rel_gap = fabs(t.pval - t.dval) / (1.0 + fabs(t.pval) + fabs(t.dval));
+  LzOut lz;
+  const GOp g{P.p_up, P.p_lo, pt};
+  if (!lanczos_dev(c, P, g, eig_tol, cf.eig_max_iters, cf.eig_block_restart, lz)) return false;
+  t.dual_lambda_min = lz.lambda;
+  t.eig_products = lz.matvecs;
+  t.eig_trusted = lz.converged;
+  t.rel_dfeas = fmax(0.0, -t.dual_lambda_min) / (1.0 + I.norm_C1);
+  t.done = t.eig_trusted && t.rel_pfeas <= cf.eps && t.rel_gap <= cf.eps && t.rel_dfeas <= cf.eps;
+  return true;
+}
+
+struct Cert {
+  Term t;
+  double pt;     // certified trace multiplier (theta) / p[m-1]
+  double theta;
+};
+
+// certify (solver.cpp:92-122)
+template <int S>
+__device__ __noinline__ bool certify_dev(Ctx& c, const Params& P, const double* U, int s, double pt,
+                            double theta, double eig_tol, Cert& ct) {
+  const DevPairs& I = P.I;
+  ct.pt = pt;
+  ct.theta = theta;
+  if (is_theta(I) && theta > 0) {
+    ct.pt = ct.pt + theta;
+    ct.theta = 0.0;
+  }
+  if (!check_termination_dev<S>(c, P, U, s, ct.pt, ct.theta, eig_tol, ct.t)) return false;
+  if (!ct.t.eig_trusted) return true;
+  Term& t = ct.t;
+  if (is_theta(I)) {
+    if (t.dual_lambda_min < 0) {
+      ct.pt = ct.pt - t.dual_lambda_min;
+      t.dval = t.dval + t.dual_lambda_min * I.b_trace;
+      t.dual_lambda_min = 0.0;
+      t.rel_dfeas = 0.0;
+    }
+  } else {
+    const double tight = fmax(0.0, -t.dual_lambda_min);
+    t.dval = t.dval + (ct.theta - tight);
+    ct.theta = tight;
+  }
+  t.rel_gap = fabs(t.pval - t.dval) / (1.0 + fabs(t.pval) + fabs(t.dval));
+  t.done = t.rel_pfeas <= P.cfg.eps && t.rel_gap <= P.cfg.eps && t.rel_dfeas <= P.cfg.eps;
+  return true;
+}
+
+// solve (solver.cpp:136-279) from buffers[0] (rank P.s_in) and the
+// multiplier already loaded into p_up / p_lo / P.p_trace.
+__device__ __noinline__ void solve_dev(Ctx& c, const Params& P, SolveOut* so) {
+  const DevPairs& I = P.I;
+  const Cfg& cf = P.cfg;
+  const double t0 = team_now(c);
+  const double deadline = t0 + cf.time_limit * 1e9;
+  const double nb1 = I.norm_b1, nb2 = I.nb2;
+  const double eps_floor = cf.eps_floor > 0 ? cf.eps_floor : cf.eps * (1.0 + nb1) / 10.0;
+  double eps_t = cf.eps0 > 0 ? cf.eps0 : 1e-2 * (1.0 + nb1);
+  eps_t = fmax(eps_t, eps_floor);
+  double beta = cf.beta0 > 0 ? cf.beta0 : 10.0 * fmax(1.0, nb2 > 0 ? 1.0 / nb2 : 1.0);
+  const double eig_term_tol = fmin(cf.eig_tol, 1e-7);
+
+  Roles R{0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10};
+  int s = P.s_in;
+  double theta = 0.0;
+  c.p_trace = P.p_trace;
+  SolveOut o{};
+  o.status = 1;
+  bool have_cert = false;
+  Cert fc;
+  double prev_pfeas = INFINITY;
+  int status = 1;  // iteration limit
+  bool nan_report = false;
+  bool numerical = false;
+
+  for (int t = 1; t <= cf.max_outer; ++t) {
+    if (team_now(c) >= deadline) {
+      status = 2;
+      break;
+    }
+    // hlr_solve takes U by value
+    HALLAR_DISPATCH_S(s, copy_rows<S_>(c, P.buf[R.rep], P.buf[R.yt], s));
+    __syncthreads();
+    c.beta = beta;
+    HlrOut ho;
+    if (!hlr_dev(c, P, R, s, beta, eps_t, t, (unsigned long long)deadline, ho)) {
+      if (c.status == kErrNumerical) {
+        numerical = true;
+        c.status = kOk;  // caught: finish(kNumericalFailure)
+        status = 3;
+        o.outer_iters = o.outer_iters;  // unchanged
+        break;
+      }
+      break;  // input / capacity errors propagate
+    }
+    o.outer_iters = t;
+    o.fw_steps += ho.fw_steps;
+    o.aipp_iters += ho.aipp_iters;
+    o.fista_iters += ho.fista_iters;
+    o.eig_products += ho.eig_products;
+    // rep.U = out.U
+    {
+      const int tb = R.rep;
+      R.rep = ho.y_buf;
+      // keep the role permutation a bijection
+      if (R.yt == ho.y_buf) R.yt = tb;
+      else if (R.wp == ho.y_buf) R.wp = tb;
+      else if (R.best == ho.y_buf) R.best = tb;
+      else if (R.x == ho.y_buf) R.x = tb;
+      else if (R.y == ho.y_buf) R.y = tb;
+      else if (R.xt == ho.y_buf) R.xt = tb;
+      else if (R.gt == ho.y_buf) R.gt = tb;
+      else if (R.yn == ho.y_buf) R.yn = tb;
+      else if (R.v == ho.y_buf) R.v = tb;
+      else if (R.tmp == ho.y_buf) R.tmp = tb;
+      s = ho.s;
+    }
+    // multiplier_update (solver.cpp:44-49): p <- p + beta r ; b.p ; finiteness
+    double bp = 0.0, bad = 0.0;
+    {
+      for (int64_t k = c.kl + threadIdx.x; k < c.kh; k += kThreads) {
+        const double pn = P.p_up[k] + beta * P.r_up[k];
+        P.p_up[k] = pn;
+        if (!isfinite(pn)) bad = 1.0;
+        if (I.b_up) bp = bp + I.b_up[k] * pn;
+      }
+      const int64_t lo_n = I.lo_ptr[c.rh] - I.lo_ptr[c.rl];
+      const int64_t lo0 = I.lo_ptr[c.rl];
+      for (int64_t e = threadIdx.x; e < lo_n; e += kThreads)
+        P.p_lo[lo0 + e] = P.p_lo[lo0 + e] + beta * P.r_lo[lo0 + e];
+      const double* U = P.buf[R.rep];
+      for (int64_t a = c.rl + threadIdx.x; a < c.rh; a += kThreads)
+        for (int k = 0; k < s; ++k)
+          if (!isfinite(U[a * s + k])) bad = 1.0;
+      double v[2] = {bp, bad};
+      team_sum<2>(c.t, c.rs, v);
+      bp = v[0];
+      bad = v[1];
+    }
+    c.p_trace = c.p_trace + beta * ho.rt;
+    theta = ho.theta;
+    if (is_theta(I) && !isfinite(c.p_trace)) bad = 1.0;
+    if (bad != 0.0) {
+      c.msg = kMsgNonFinite;
+      status = 3;
+      nan_report = true;
+      break;
+    }
+    const double rel_pfeas = sqrt(ho.rr) / (1.0 + nb1);
+    const double pval = ho.cdot;
+    const double bpa = is_theta(I) ? bp + I.b_trace * c.p_trace : bp;
+    const double dval = -bpa - ho.theta;
+    const double rel_gap = fabs(pval - dval) / (1.0 + fabs(pval) + fabs(dval));
+    const double lam = is_theta(I) ? ho.lambda_min + ho.theta : ho.lambda_min;
+    const double rel_dfeas_est = fmax(0.0, -lam) / (1.0 + I.norm_C1);
+    {
+      TraceEv ev{};
+      ev.kind = 2;
+      ev.outer_iter = t;
+      ev.beta = beta;
+      ev.eps_inner = eps_t;
+      ev.gap = ho.gap;
+      ev.theta = ho.theta;
+      ev.rank = s;
+      ev.al_value = ho.al_val;
+      ev.rel_pfeas = rel_pfeas;
+      ev.rel_gap = rel_gap;
+      ev.rel_dfeas = rel_dfeas_est;
+      emit_trace(P, c, ev);
+    }
+    if (ho.eig_trusted && rel_pfeas <= cf.eps && rel_gap <= cf.eps && rel_dfeas_est <= cf.eps) {
+      Cert ct;
+      bool ok = true;
+      HALLAR_DISPATCH_S(s, ok = certify_dev<S_>(c, P, P.buf[R.rep], s, c.p_trace, theta,
+                                                eig_term_tol, ct));
+      if (!ok) break;
+      o.eig_products += ct.t.eig_products;
+      if (ct.t.done) {
+        fc = ct;
+        have_cert = true;
+        status = 0;
+        break;
+      }
+    }
+    if (rel_pfeas > 0.9 * prev_pfeas) beta *= cf.beta_growth;
+    prev_pfeas = rel_pfeas;
+    eps_t = fmax(eps_floor, eps_t * cf.eps_decay);
+  }
+  if (c.status != kOk) {
+    if (c.t.rank == 0 && threadIdx.x == 0) {
+      so->status = c.status;
+      so->msg = c.msg;
+    }
+    return;
+  }
+  (void)numerical;
+  // finish() (solver.cpp:175-202)
+  if (!have_cert && !nan_report) {
+    Cert ct;
+    bool ok = true;
+    HALLAR_DISPATCH_S(s, ok = certify_dev<S_>(c, P, P.buf[R.rep], s, c.p_trace, theta,
+                                              eig_term_tol, ct));
+    if (!ok) {
+      if (c.t.rank == 0 && threadIdx.x == 0) {
+        so->status = c.status;
+        so->msg = c.msg;
+      }
+      return;
+    }
+    o.eig_products += ct.t.eig_products;
+    fc = ct;
+    have_cert = true;
+  }
+  o.out_buf = R.rep;
+  o.rank = s;
+  o.msg = c.msg;
+  if (nan_report) {
+    o.status = 3;
+    o.pval = o.dval = o.dval_no_theta = NAN;
+    o.rel_pfeas = o.rel_gap = o.rel_dfeas = NAN;
+    o.theta = theta;
+    o.p_trace = c.p_trace;
+  } else {
+    o.status = status;
+    o.theta = fc.theta;
+    o.p_trace = fc.pt;
+    o.rel_pfeas = fc.t.rel_pfeas;
+    o.rel_gap = fc.t.rel_gap;
+    o.rel_dfeas = fc.t.rel_dfeas;
+    o.pval = fc.t.pval;  // scaled units; host multiplies by tau
+    o.dval = fc.t.dval;
+    const double bpa = is_theta(I) ? fc.t.bp_edges + I.b_trace * fc.pt : fc.t.bp_edges;
+    o.dval_no_theta = -bpa;
+  }
+  if (c.t.rank == 0 && threadIdx.x == 0) *so = o;
+}
+
+// ----------------------------------------------------------------- ops ----
+template <int S>
+__device__ __noinline__ void op_dispatch(Ctx& c, const Params& P, SolveOut* so) {
+  const DevPairs& I = P.I;
+  const int s = P.s_in;
+  const double* U = P.buf[0];
+  c.beta = P.beta_in;
+  c.p_trace = P.p_trace;
+  switch (P.op) {
+    case kOpMap: {
+      double nrm2;
+      factor_stats<S>(c, P, U, s, &nrm2);
+      double ms[2];
+      map_pass<S>(c, P, U, s, kMapOut, nullptr, P.out_vec, nullptr, ms);
+      if (is_theta(I) && c.t.rank == 0 && threadIdx.x == 0) P.out_vec[I.np] = nrm2;
+      break;
+    }
+    case kOpCPlusAdj:
+    case kOpAdj: {
+      double nrm2;
+      factor_stats<S>(c, P, U, s, &nrm2);
+      const bool withC = P.op == kOpCPlusAdj;
+      double* out = P.out_mat;
+      auto epi = [&](int64_t a, double h, double) {
+        if (c.lane < s) out[a * s + c.lane] = h;
+      };
+      double sums[3] = {0, 0, 0};
+      const double alpha = is_theta(I) ? P.q_trace_in : 0.5;
+      const bool zero = !is_theta(I) && !withC;
+      row_pass<S, true>(c, P, U, s, P.q_up, P.q_lo, 0.0, alpha,
+                        (is_theta(I) && withC) ? c.cs : nullptr, zero, sums, epi);
+      break;
+    }
+    case kOpApplyC: {
+      double nrm2;
+      factor_stats<S>(c, P, U, s, &nrm2);
+      for (int64_t a = c.rl + threadIdx.x; a < c.rh; a += kThreads)
+        for (int k = 0; k < s; ++k)
+          P.out_mat[a * s + k] = is_theta(I) ? -1.0 * c.cs[k] : 0.5 * U[a * s + k];
+      break;
+    }
+    case kOpAlValue: {
+      double val;
+      if (al_value_dev<S>(c, P, U, s, P.p_up, P.p_trace, P.beta_in, &val, nullptr) &&
+          c.t.rank == 0 && threadIdx.x == 0)
+        P.scalars[0] = val;
+      break;
+    }
+    case kOpAlValGrad:
+    case kOpAlGrad: {
+      double nrm2;
+      factor_stats<S>(c, P, U, s, &nrm2);
+      const double beta = P.beta_in;
+      double rt = 0.0, qt = 0.0;
+      if (is_theta(I)) {
+        rt = nrm2 - I.b_trace;
+        qt = P.p_trace + beta * rt;
+      }
+      double hU = 0.0, bad = 0.0;
+      double* out = P.out_mat;
+      auto epi = [&](int64_t a, double h, double uo) {
+        if (c.lane < s) {
+          hU = hU + h * uo;
+          const double g = 2.0 * h;
+          if (!isfinite(g)) bad = 1.0;
+          out[a * s + c.lane] = g;
+        }
+      };
+      double sums[3] = {0, 0, 0};
+      row_pass<S, false>(c, P, U, s, P.p_up, P.p_lo, beta, theta_alpha_or_half(I, qt),
+                         is_theta(I) ? c.cs : nullptr, false, sums, epi);
+      double v[5] = {hU, sums[0], sums[1], sums[2], bad};
+      team_sum<5>(c.t, c.rs, v);
+      double pr = v[1], rr = v[2], qrb = v[3];
+      if (is_theta(I)) {
+        pr = pr + P.p_trace * rt;
+        rr = rr + rt * rt;
+        qrb = qrb + qt * (rt + I.b_trace);
+      }
+      const double val = (v[0] - qrb) + pr + 0.5 * beta * rr;
+      if (P.op == kOpAlValGrad) {
+        if (!isfinite(val)) fail(c, kErrNumerical, kMsgAlValGrad);
+        if (c.t.rank == 0 && threadIdx.x == 0) P.scalars[0] = val;
+      } else if (v[4] != 0.0) {
+        fail(c, kErrNumerical, kMsgAlGrad);
+      }
+      break;
+    }
+    case kOpMinEigG: {
+      double pr, rr, rt, qt;
+      if (!gradop_dev<S>(c, P, U, s, P.beta_in, &pr, &rr, &rt, &qt)) break;
+      const GOp g{P.q_up, P.q_lo, qt};
+      LzOut lz;
+      if (!lanczos_dev(c, P, g, P.rho_in, P.cfg.eig_max_iters, P.cfg.eig_block_restart, lz)) break;
+      if (lz.vslot >= 0) {
+        const double* v = slot_ptr(P, lz.vslot);
+        for (int64_t a = c.rl + threadIdx.x; a < c.rh; a += kThreads) P.out_vec[a] = v[a];
+      }
+      if (c.t.rank == 0 && threadIdx.x == 0) {
+        P.scalars[0] = lz.lambda;
+        P.scalars[1] = lz.residual;
+        P.iscalars[0] = lz.matvecs;
+        P.iscalars[1] = lz.converged ? 1 : 0;
+      }
+      break;
+    }
+    case kOpAipp: {
+      Roles R{10, 0, 1, 2, 3, 4, 5, 6, 7, 8, 9};
+      AippOut ao;
+      if (!aipp_dev<S>(c, P, R, s, P.rho_in, ao)) break;
+      const double* W = P.buf[ao.w_buf];
+      for (int64_t a = c.rl + threadIdx.x; a < c.rh; a += kThreads)
+        for (int k = 0; k < s; ++k) P.out_mat[a * s + k] = W[a * s + k];
+      if (c.t.rank == 0 && threadIdx.x == 0) {
+        P.scalars[0] = ao.R_norm;
+        P.scalars[1] = ao.g_value;
+        P.scalars[2] = ao.lambda;
+        P.iscalars[0] = ao.status;
+        P.iscalars[1] = ao.prox_iters;
+        P.iscalars[2] = ao.fista_iters;
+      }
+      break;
+    }
+    default:
+      break;
+  }
+  if (c.t.rank == 0 && threadIdx.x == 0) {
+    so->status = c.status;
+    so->msg = c.msg;
+  }
+}
+
+}  // namespace hallar

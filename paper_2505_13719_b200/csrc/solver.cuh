@@ -1,0 +1,700 @@
+// Device Lanczos (with the CTA-parallel Jacobi eigen-solver), HLR inner
+// method, outer AL driver and certificate, and the op dispatcher of the
+// persistent kernel.  Continues device.cuh.
+#pragma once
+
+#include "device.cuh"
+
+namespace hallar {
+
+#define HALLAR_DISPATCH_S(s, CALL)        \
+  switch (s) {                            \
+    case 1: { constexpr int S_ = 1; CALL; } break; \
+    case 2: { constexpr int S_ = 2; CALL; } break; \
+    case 3: { constexpr int S_ = 3; CALL; } break; \
+    case 4: { constexpr int S_ = 4; CALL; } break; \
+    default: { constexpr int S_ = 0; CALL; } break; \
+  }
+
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+// Team-consistent clock: CTA 0's timer, broadcast through a reduction.
+__device__ __noinline__ double team_now(Ctx& c) {
+  double v[1] = {(c.t.rank == 0 && threadIdx.x == 0) ? (double)globaltimer_ns() : 0.0};
+  team_sum<1>(c.t, c.rs, v);
+  return v[0];
+}
+
+__device__ void emit_trace(const Params& P, Ctx& c, const TraceEv& ev) {
+  if (!P.cfg.trace || c.t.rank != 0 || threadIdx.x != 0 || !P.trace) return;
+  const int i = *P.trace_count;
+  if (i < P.trace_cap) P.trace[i] = ev;
+  *P.trace_count = i + 1;
+}
+
+// ---------------------------------------------------------------- Jacobi ---
+// Same rotations, same order, same arithmetic as oracle/src/base.cpp
+// jacobi_eigh: tournament rounds; all row rotations, then column rotations,
+// then pivots zeroed.  Input H column-major with leading dim ldh; outputs
+// ascending c.ev[0..k) and c.E (column-major, ld k), signs normalised.
+__device__ __noinline__ void jacobi_dev(Ctx& c, const double* H, int ldh, int k) {
+  double* A = c.JA;
+  double* V = c.JV;
+  const int tid = threadIdx.x;
+  for (int idx = tid; idx < k * k; idx += kThreads) {
+    const int i = idx % k, j = idx / k;
+    A[idx] = H[i + j * ldh];
+    V[idx] = (i == j) ? 1.0 : 0.0;
+  }
+  __syncthreads();
+  double* red = c.rs.part;  // scratch [kWarps]
+  auto block_max = [&](double v) -> double {
+    v = warp_max(v);
+    if (c.lane == 0) red[c.warp] = v;
+    __syncthreads();
+    double m = red[0];
+    for (int w = 1; w < kWarps; ++w) m = fmax(m, red[w]);
+    __syncthreads();
+    return m;
+  };
+  if (k > 1) {
+    const int kp = k + (k & 1);
+    double mloc = 0.0;
+    for (int idx = tid; idx < k * k; idx += kThreads) mloc = fmax(mloc, fabs(A[idx]));
+    const double scale = block_max(mloc);
+    const double thresh = scale * 1e-18;
+    for (int sweep = 0; sweep < 40; ++sweep) {
+      double oloc = 0.0;
+      for (int idx = tid; idx < k * k; idx += kThreads) {
+        const int i = idx % k, j = idx / k;
+        if (i < j) oloc = fmax(oloc, fabs(A[idx]));
+      }
+      const double off = block_max(oloc);
+      if (off <= thresh || off == 0.0) break;
+      for (int round = 0; round < kp - 1; ++round) {
+        if (tid == 0) {
+          int np = 0;
+          for (int t = 0; t < kp / 2; ++t) {
+            const int pa = t == 0 ? 0 : 1 + (t - 1 + round) % (kp - 1);
+            const int tb = kp - 1 - t;
+            const int pb = tb == 0 ? 0 : 1 + (tb - 1 + round) % (kp - 1);
+            int x = pa, y = pb;
+            if (x >= k || y >= k) continue;
+            if (x > y) { const int z = x; x = y; y = z; }
+            c.jpq[2 * np] = x;
+            c.jpq[2 * np + 1] = y;
+            ++np;
+          }
+          c.jpq[2 * 16] = np;
+        }
+        __syncthreads();
+        const int np = c.jpq[32];
+        if (tid < np) {
+          const int p = c.jpq[2 * tid], q = c.jpq[2 * tid + 1];
+          const double apq = A[p + q * k];
+          double cc = 1.0, ss = 0.0;
+          if (apq != 0.0) {
+            const double th = (A[q + q * k] - A[p + p * k]) / (2.0 * apq);
+            double tn;
+            if (fabs(th) > 1e150)
+              tn = 0.5 / th;
+            else
+              tn = (th >= 0.0 ? 1.0 : -1.0) / (fabs(th) + sqrt(th * th + 1.0));
+            cc = 1.0 / sqrt(tn * tn + 1.0);
+            ss = tn * cc;
+          }
+          c.jcs[2 * tid] = cc;
+          c.jcs[2 * tid + 1] = ss;
+        }
+        __syncthreads();
+        for (int idx = tid; idx < np * k; idx += kThreads) {  // rows
+          const int t = idx / k, j = idx % k;
+          const double cc = c.jcs[2 * t], ss = c.jcs[2 * t + 1];
+          if (ss == 0.0) continue;
+          const int p = c.jpq[2 * t], q = c.jpq[2 * t + 1];
+          const double ap = A[p + j * k], aq = A[q + j * k];
+          A[p + j * k] = cc * ap - ss * aq;
+          A[q + j * k] = ss * ap + cc * aq;
+        }
+        __syncthreads();
+        for (int idx = tid; idx < np * k; idx += kThreads) {  // columns + vectors
+          const int t = idx / k, i = idx % k;
+          const double cc = c.jcs[2 * t], ss = c.jcs[2 * t + 1];
+          if (ss == 0.0) continue;
+          const int p = c.jpq[2 * t], q = c.jpq[2 * t + 1];
+          const double ap = A[i + p * k], aq = A[i + q * k];
+          A[i + p * k] = cc * ap - ss * aq;
+          A[i + q * k] = ss * ap + cc * aq;
+          const double vp = V[i + p * k], vq = V[i + q * k];
+          V[i + p * k] = cc * vp - ss * vq;
+          V[i + q * k] = ss * vp + cc * vq;
+        }
+        __syncthreads();
+        if (tid < np && c.jcs[2 * tid + 1] != 0.0) {
+          const int p = c.jpq[2 * tid], q = c.jpq[2 * tid + 1];
+          A[p + q * k] = 0.0;
+          A[q + p * k] = 0.0;
+        }
+        __syncthreads();
+      }
+    }
+  }
+  // stable ascending ranks; sign: largest-|.| (first on ties) positive
+  if (tid < k) {
+    const double d = A[tid + tid * k];
+    int rk = 0;
+    for (int j = 0; j < k; ++j) {
+      const double dj = A[j + j * k];
+      if (dj < d || (dj == d && j < tid)) ++rk;
+    }
+    int imax = 0;
+    double best = -1.0;
+    for (int i = 0; i < k; ++i)
+      if (fabs(V[i + tid * k]) > best) {
+        best = fabs(V[i + tid * k]);
+        imax = i;
+      }
+    const double sg = V[imax + tid * k] < 0.0 ? -1.0 : 1.0;
+    c.ev[rk] = d;
+    for (int i = 0; i < k; ++i) c.E[i + rk * k] = sg * V[i + tid * k];
+  }
+  __syncthreads();
+}
+
+// --------------------------------------------------------------- Lanczos ---
+struct GOp {
+  const double* qup;
+  const double* qlo;
+  double qt;
+};
+struct LzOut {
+  double lambda = 0.0, residual = INFINITY;
+  int matvecs = 0;
+  bool converged = false;
+  int vslot = -1;
+};
+
+__device__ __forceinline__ double* slot_ptr(const Params& P, int sl) {
+  return P.vslot + (size_t)sl * P.I.n;
+}
+
+// dst = -(C v + A*(q) v) for v in slot sv (apply_B, lanczos.cpp:38); the
+// caller has team-synchronised after v was written.
+__device__ __noinline__ void lz_apply(Ctx& c, const Params& P, const GOp& g, int sv, double* dst) {
+  const DevPairs& I = P.I;
+  const double* v = slot_ptr(P, sv);
+  auto epi = [&](int64_t a, double h, double) {
+    if (c.lane == 0) dst[a] = -h;
+  };
+  double sums[3] = {0.0, 0.0, 0.0};
+  row_pass<1, true>(c, P, v, 1, g.qup, g.qlo, 0.0, theta_alpha_or_half(I, g.qt),
+                    is_theta(I) ? &c.vsum[sv] : nullptr, false, sums, epi);
+  __syncthreads();
+}
+
+// h[i] = V_i . w for i < k  (result in c.rs.out[0..k))
+__device__ __noinline__ void lz_dot(Ctx& c, const Params& P, int k, const double* w) {
+  double mine = 0.0;
+  for (int64_t a0 = c.rl + c.warp * 32; a0 < c.rh; a0 += kWarps * 32) {
+    const int64_t a = a0 + c.lane;
+    const bool ok = a < c.rh;
+    const double wa = ok ? w[a] : 0.0;
+    for (int i = 0; i < k; ++i) {
+      double t = ok ? slot_ptr(P, c.col[i])[a] * wa : 0.0;
+      t = warp_sum(t);
+      if (c.lane == i) mine = mine + t;
+    }
+  }
+  team_sum_lanes(c.t, c.rs, mine, k);
+}
+// w -= V_k h; then (dot_after) h2 = V_k' w  or  ||w||^2.  h read from smem.
+__device__ __noinline__ void lz_sub(Ctx& c, const Params& P, int k, double* w, const double* h,
+                       bool dot_after) {
+  double mine = 0.0;
+  for (int64_t a0 = c.rl + c.warp * 32; a0 < c.rh; a0 += kWarps * 32) {
+    const int64_t a = a0 + c.lane;
+    const bool ok = a < c.rh;
+    double wn = 0.0;
+    if (ok) {
+      double s = 0.0;
+      for (int i = 0; i < k; ++i) s = s + slot_ptr(P, c.col[i])[a] * h[i];
+      wn = w[a] - s;
+      w[a] = wn;
+    }
+    if (dot_after) {
+      for (int i = 0; i < k; ++i) {
+        double t = ok ? slot_ptr(P, c.col[i])[a] * wn : 0.0;
+        t = warp_sum(t);
+        if (c.lane == i) mine = mine + t;
+      }
+    } else {
+      mine = mine + wn * wn;
+    }
+  }
+  if (dot_after) {
+    team_sum_lanes(c.t, c.rs, mine, k);
+  } else {
+    double v[1] = {mine};
+    team_sum<1>(c.t, c.rs, v);
+  }
+}
+// orthogonalize (lanczos.cpp:22-28): h <- V'w; w -= Vh; h2 <- V'w; w -= Vh2;
+// h += h2.  Returns ||w||^2; h left in hh[0..k).
+__device__ __noinline__ double lz_cgs2(Ctx& c, const Params& P, int k, double* w, double* hh, double* hh2) {
+  lz_dot(c, P, k, w);
+  if (threadIdx.x < (unsigned)k) hh[threadIdx.x] = c.rs.out[threadIdx.x];
+  __syncthreads();
+  lz_sub(c, P, k, w, hh, true);
+  if (threadIdx.x < (unsigned)k) hh2[threadIdx.x] = c.rs.out[threadIdx.x];
+  __syncthreads();
+  lz_sub(c, P, k, w, hh2, false);
+  const double ww = c.rs.out[0];
+  __syncthreads();
+  if (threadIdx.x < (unsigned)k) hh[threadIdx.x] = hh[threadIdx.x] + hh2[threadIdx.x];
+  __syncthreads();
+  return ww;
+}
+// slot dst = src / nrm ; vsum[dst] = sum (team-reduced)
+__device__ __noinline__ void lz_scale_into(Ctx& c, const Params& P, const double* src, double nrm, int dst) {
+  double* d = slot_ptr(P, dst);
+  double v[1] = {0.0};
+  for (int64_t a = c.rl + threadIdx.x; a < c.rh; a += kThreads) {
+    const double x = src[a] / nrm;
+    d[a] = x;
+    v[0] = v[0] + x;
+  }
+  team_sum<1>(c.t, c.rs, v);
+  if (threadIdx.x == 0) c.vsum[dst] = v[0];
+  __syncthreads();
+}
+// slot dst = V_f e (e in smem, column of c.E); returns ||.||^2
+__device__ __noinline__ double lz_combine(Ctx& c, const Params& P, int f, const double* e, int dst) {
+  double* d = slot_ptr(P, dst);
+  double v[1] = {0.0};
+  for (int64_t a = c.rl + threadIdx.x; a < c.rh; a += kThreads) {
+    double s = 0.0;
+    for (int i = 0; i < f; ++i) s = s + slot_ptr(P, c.col[i])[a] * e[i];
+    d[a] = s;
+    v[0] = v[0] + s * s;
+  }
+  team_sum<1>(c.t, c.rs, v);
+  return v[0];
+}
+
+// min_eigenpair (lanczos.cpp:32-141) of op = C + A*(q), i.e. B = -op.
+// Slots used: c.col[] basis, plus scratch; returns the best pair's slot.
+__device__ __noinline__ bool lanczos_dev(Ctx& c, const Params& P, const GOp& g, double tol, int max_iters,
+                            int block_restart, LzOut& best) {
+  const DevPairs& I = P.I;
+  const int64_t n = I.n;
+  const int kmax = (int)min((int64_t)block_restart, n);
+  const int keep = max(1, kmax / 3);
+  double* hh = c.hh;
+  double* hh2 = c.hh2;
+  unsigned long long used = 0ull;
+  auto alloc = [&]() -> int {
+    for (int sl = 0; sl < P.nslot; ++sl)
+      if (!((used >> sl) & 1ull)) {
+        used |= 1ull << sl;
+        return sl;
+      }
+    return -1;
+  };
+  auto release = [&](int sl) {
+    if (sl >= 0) used &= ~(1ull << sl);
+  };
+  int refill = 0;
+  // V(:,0) = v0/|v0|
+  {
+    double v[1] = {0.0};
+    for (int64_t a = c.rl + threadIdx.x; a < c.rh; a += kThreads) {
+      const double x = P.lz_rand[a];
+      v[0] = v[0] + x * x;
+    }
+    team_sum<1>(c.t, c.rs, v);
+    const int s0 = alloc();
+    if (threadIdx.x == 0) c.col[0] = s0;
+    __syncthreads();
+    lz_scale_into(c, P, P.lz_rand, sqrt(v[0]), s0);
+  }
+  for (int idx = threadIdx.x; idx < kHLd * kHLd; idx += kThreads) c.H[idx] = 0.0;
+  __syncthreads();
+  int matvecs = 0, basis = 1, filled = 0;
+  double beta = 0.0;
+  best = LzOut();
+  best.residual = INFINITY;
+  const int wslot = alloc();  // holds w across restarts
+  double* w = slot_ptr(P, wslot);
+
+  for (;;) {
+    bool breakdown = false;
+    while (filled < basis && matvecs < max_iters) {
+      const int j = filled;
+      lz_apply(c, P, g, c.col[j], w);
+      ++matvecs;
+      const double ww = lz_cgs2(c, P, basis, w, hh, hh2);
+      if (threadIdx.x < (unsigned)basis) {
+        c.H[threadIdx.x + j * kHLd] = hh[threadIdx.x];
+        c.H[j + threadIdx.x * kHLd] = hh[threadIdx.x];
+      }
+      __syncthreads();
+      ++filled;
+      beta = sqrt(ww);
+      double hmax = 0.0;
+      for (int t = 0; t < basis; ++t) hmax = fmax(hmax, fabs(hh[t]));
+      if (beta <= 1e-13 * fmax(1.0, hmax)) {
+        breakdown = true;
+        break;
+      }
+      if (basis < kmax) {
+        const int sl = alloc();
+        if (threadIdx.x == 0) {
+          c.col[basis] = sl;
+          c.H[basis + j * kHLd] = beta;
+          c.H[j + basis * kHLd] = beta;
+        }
+        __syncthreads();
+        lz_scale_into(c, P, w, beta, sl);
+        ++basis;
+      }
+    }
+    const int f = filled;
+    jacobi_dev(c, c.H, kHLd, f);
+    const int top = f - 1;
+    const double mu = c.ev[top];
+    const double res_est = breakdown ? 0.0 : beta * fabs(c.E[(f - 1) + top * f]);
+    const bool budget_left = matvecs + 1 < max_iters;
+    if (res_est <= tol * fmax(1.0, fabs(mu)) || !budget_left || (breakdown && filled >= n)) {
+      // measure(V_f * e_top)
+      const int xs = alloc();
+      const double nx2 = lz_combine(c, P, f, c.E + top * f, xs);
+      {
+        double* x = slot_ptr(P, xs);
+        const double nx = sqrt(nx2);
+        double v[1] = {0.0};
+        for (int64_t a = c.rl + threadIdx.x; a < c.rh; a += kThreads) {
+          const double t = x[a] / nx;
+          x[a] = t;
+          v[0] = v[0] + t;
+        }
+        team_sum<1>(c.t, c.rs, v);
+        if (threadIdx.x == 0) c.vsum[xs] = v[0];
+        __syncthreads();
+      }
+      const int bs = alloc();
+      double* Bx = slot_ptr(P, bs);
+      lz_apply(c, P, g, xs, Bx);
+      ++matvecs;
+      const double* x = slot_ptr(P, xs);
+      double v1[1] = {0.0};
+      for (int64_t a = c.rl + threadIdx.x; a < c.rh; a += kThreads) v1[0] = v1[0] + x[a] * Bx[a];
+      team_sum<1>(c.t, c.rs, v1);
+      const double mux = v1[0];
+      double v2[1] = {0.0};
+      for (int64_t a = c.rl + threadIdx.x; a < c.rh; a += kThreads) {
+        const double d = Bx[a] - mux * x[a];
+        v2[0] = v2[0] + d * d;
+      }
+      team_sum<1>(c.t, c.rs, v2);
+      release(bs);
+      LzOut o;
+      o.lambda = -mux;
+      o.residual = sqrt(v2[0]);
+      o.matvecs = matvecs;
+      o.converged = o.residual <= tol * fmax(1.0, fabs(o.lambda));
+      o.vslot = xs;
+      if (o.residual < best.residual) {
+        release(best.vslot);
+        best = o;
+      } else {
+        release(xs);
+      }
+      best.matvecs = matvecs;
+      if (best.converged || matvecs >= max_iters || (breakdown && filled >= n)) {
+        best.matvecs = matvecs;
+        return true;
+      }
+    }
+    // thick restart
+    const int l = min(keep, f - 1 > 0 ? f - 1 : 1);
+    int newcol[kLanczosMax];
+    {
+      for (int t = 0; t < l; ++t) newcol[t] = alloc();
+      if (newcol[l - 1] < 0) {
+        fail(c, kErrCapacity, kMsgRefillCap);
+        return false;
+      }
+      // kept_t = V_f E[:, f-1-t], column sums per t
+      double mine = 0.0;
+      for (int64_t a0 = c.rl + c.warp * 32; a0 < c.rh; a0 += kWarps * 32) {
+        const int64_t a = a0 + c.lane;
+        const bool ok = a < c.rh;
+        for (int t = 0; t < l; ++t) {
+          double s = 0.0;
+          if (ok) {
+            const double* e = c.E + (f - 1 - t) * f;
+            for (int i = 0; i < f; ++i) s = s + slot_ptr(P, c.col[i])[a] * e[i];
+            slot_ptr(P, newcol[t])[a] = s;
+          }
+          const double ts = warp_sum(s);
+          if (c.lane == t) mine = mine + ts;
+        }
+      }
+      team_sum_lanes(c.t, c.rs, mine, l);
+      if (threadIdx.x < (unsigned)l) c.vsum[newcol[threadIdx.x]] = c.rs.out[threadIdx.x];
+      __syncthreads();
+    }
+    for (int t = 0; t < basis; ++t) release(c.col[t]);
+    for (int idx = threadIdx.x; idx < kHLd * kHLd; idx += kThreads) c.H[idx] = 0.0;
+    __syncthreads();
+    if (threadIdx.x < (unsigned)l) {
+      c.H[threadIdx.x + threadIdx.x * kHLd] = c.ev[f - 1 - threadIdx.x];
+      c.col[threadIdx.x] = newcol[threadIdx.x];
+    }
+    __syncthreads();
+    const int sl = alloc();
+    if (breakdown) {
+      if (refill >= P.n_refill) {
+        fail(c, kErrCapacity, kMsgRefillCap);
+        return false;
+      }
+      ++refill;
+      const double* fr = P.lz_rand + (size_t)refill * n;
+      for (int64_t a = c.rl + threadIdx.x; a < c.rh; a += kThreads) w[a] = fr[a];
+      __syncthreads();
+      const double fn2 = lz_cgs2(c, P, l, w, hh, hh2);
+      const double fn = sqrt(fn2);
+      if (fn <= 1e-13) {
+        best.matvecs = matvecs;
+        return true;
+      }
+      if (threadIdx.x == 0) c.col[l] = sl;
+      __syncthreads();
+      lz_scale_into(c, P, w, fn, sl);
+    } else {
+      if (threadIdx.x == 0) c.col[l] = sl;
+      __syncthreads();
+      lz_scale_into(c, P, w, beta, sl);
+    }
+    basis = l + 1;
+    filled = l;
+  }
+}
+
+// -------------------------------------------------------------------- HLR ---
+struct HlrOut {
+  int y_buf = 0, s = 1;
+  double theta = 0, gap = 0, lambda_min = 0, al_val = 0, cdot = 0;
+  double pr = 0, rr = 0, rt = 0;  // residual stats at exit (incl. trace)
+  bool eig_trusted = true;
+  int status = 0;
+  long long aipp_iters = 0, fista_iters = 0, eig_products = 0;
+  int fw_steps = 0;
+};
+
+// GradientOperator(Y): writes q/r arrays; returns p.r, ||r||^2 (incl. trace),
+// and the trace residual / multiplier.
+template <int S>
+__device__ __noinline__ bool gradop_dev(Ctx& c, const Params& P, const double* Y, int s, double beta,
+                           double* pr, double* rr, double* rt, double* qt) {
+  const DevPairs& I = P.I;
+  double ny2;
+  factor_stats<S>(c, P, Y, s, &ny2);
+  double sums[2] = {0.0, 0.0};
+  bool bad = false;
+  gradop_pass<S>(c, P, Y, s, beta, sums, &bad);
+  double v[3] = {sums[0], sums[1], bad ? 1.0 : 0.0};
+  team_sum<3>(c.t, c.rs, v);
+  double p_r = v[0], r_r = v[1];
+  double r_t = 0.0, q_t = 0.0;
+  if (is_theta(I)) {
+    r_t = ny2 - I.b_trace;
+    q_t = c.p_trace + beta * r_t;
+    p_r = p_r + c.p_trace * r_t;
+    r_r = r_r + r_t * r_t;
+    if (!isfinite(q_t)) v[2] = 1.0;
+  }
+  *pr = p_r;
+  *rr = r_r;
+  *rt = r_t;
+  *qt = q_t;
+  if (v[2] != 0.0) {
+    fail(c, kErrNumerical, kMsgGradOp);
+    return false;
+  }
+  return true;
+}
+
+// <G Y, Y> with G = C + A*(q) stored (fw_gap, hlr.cpp:8-10)
+template <int S>
+__device__ __noinline__ double fw_gap_dev(Ctx& c, const Params& P, const double* Y, int s, const GOp& g) {
+  const DevPairs& I = P.I;
+  double ny2;
+  factor_stats<S>(c, P, Y, s, &ny2);
+  double gs = 0.0;
+  auto epi = [&](int64_t, double h, double yo) {
+    if (c.lane < s) gs = gs + h * yo;
+  };
+  double sums[3] = {0.0, 0.0, 0.0};
+  row_pass<S, true>(c, P, Y, s, g.qup, g.qlo, 0.0, theta_alpha_or_half(I, g.qt),
+                    is_theta(I) ? c.cs : nullptr, false, sums, epi);
+  double v[1] = {gs};
+  team_sum<1>(c.t, c.rs, v);
+  return v[0];
+}
+
+// rank_update / shrink (hlr.cpp:46-53, 127-134) into buffer dst.
+template <int S>
+__device__ __noinline__ void rank_update_dev(Ctx& c, const Params& P, const double* Y, int s, const double* y,
+                                double alpha, bool theta_pos, double* dst, int* s_new) {
+  if (theta_pos) {
+    if (alpha == 1.0) {
+      for (int64_t a = c.rl + threadIdx.x; a < c.rh; a += kThreads) dst[a] = y[a];
+      *s_new = 1;
+    } else {
+      const double sa = sqrt(1.0 - alpha), sb = sqrt(alpha);
+      const int s1 = s + 1;
+      for (int64_t a = c.rl + threadIdx.x; a < c.rh; a += kThreads) {
+        for (int k = 0; k < s; ++k) dst[a * s1 + k] = sa * Y[a * s + k];
+        dst[a * s1 + s] = sb * y[a];
+      }
+      *s_new = s1;
+    }
+  } else {
+    if (alpha == 1.0) {
+      for (int64_t a = c.rl + threadIdx.x; a < c.rh; a += kThreads) dst[a] = 0.0;
+      *s_new = 1;
+    } else {
+      const double sa = sqrt(1.0 - alpha);
+      for (int64_t a = c.rl + threadIdx.x; a < c.rh; a += kThreads)
+        for (int k = 0; k < s; ++k) dst[a * s + k] = sa * Y[a * s + k];
+      *s_new = s;
+    }
+  }
+  c.t.sync();
+}
+
+// hlr_solve (hlr.cpp:55-151).  Input buffers[R.yt] with rank s.
+__device__ __noinline__ bool hlr_dev(Ctx& c, const Params& P, Roles& R, int s, double beta, double eps_t,
+                        int outer_iter, unsigned long long deadline_ns, HlrOut& out) {
+  const DevPairs& I = P.I;
+  const Cfg& cf = P.cfg;
+  out = HlrOut();
+  for (int step = 0;; ++step) {
+    AippOut ao;
+    bool ok = true;
+    HALLAR_DISPATCH_S(s, ok = aipp_dev<S_>(c, P, R, s, eps_t, ao));
+    if (!ok) return false;
+    out.aipp_iters += ao.prox_iters;
+    out.fista_iters += ao.fista_iters;
+    const int ybuf = ao.w_buf;
+    const double* Y = P.buf[ybuf];
+    double pr = 0, rr = 0, rt = 0, qt = 0;
+    HALLAR_DISPATCH_S(s, ok = gradop_dev<S_>(c, P, Y, s, beta, &pr, &rr, &rt, &qt));
+    if (!ok) return false;
+    const GOp g{P.q_up, P.q_lo, qt};
+    LzOut lz;
+    if (!lanczos_dev(c, P, g, 0.1 * eps_t, cf.eig_max_iters, cf.eig_block_restart, lz))
+      return false;
+    out.eig_products += lz.matvecs;
+    const double theta = lz.lambda < 0 ? -lz.lambda : 0.0;
+    double gap;
+    HALLAR_DISPATCH_S(s, gap = fw_gap_dev<S_>(c, P, Y, s, g));
+    gap = gap + theta;
+    {
+      TraceEv ev{};
+      ev.kind = 0;
+      ev.outer_iter = outer_iter;
+      ev.beta = beta;
+      ev.eps_inner = eps_t;
+      ev.gap = gap;
+      ev.theta = theta;
+      ev.rank = s;
+      ev.al_value = ao.g_value;
+      emit_trace(P, c, ev);
+    }
+    const bool done = gap <= eps_t;
+    const bool no_steps = step >= cf.max_fw_steps;
+    const bool no_time = team_now(c) >= (double)deadline_ns;
+    if (done || no_steps || no_time || !lz.converged) {
+      out.y_buf = ybuf;
+      out.s = s;
+      out.theta = theta;
+      out.gap = gap;
+      out.lambda_min = lz.lambda;
+      out.al_val = ao.g_value;
+      out.pr = pr;
+      out.rr = rr;
+      out.rt = rt;
+      out.cdot = ao.g_value - pr - 0.5 * beta * rr;
+      out.eig_trusted = lz.converged;
+      out.status = done ? 0 : (no_time ? 2 : 1);
+      if (!lz.converged && !done) out.status = 1;
+      return true;
+    }
+    // fw_stepsize (hlr.cpp:31-44): numer = gap (same G, same Y)
+    const double* yv = theta > 0 ? slot_ptr(P, lz.vslot) : nullptr;
+    double denom;
+    {
+      double v[2] = {0.0, 0.0};
+      if (yv)
+        for (int64_t a = c.rl + threadIdx.x; a < c.rh; a += kThreads) v[0] = v[0] + yv[a] * yv[a];
+      for (int64_t k = c.kl + threadIdx.x; k < c.kh; k += kThreads) {
+        const double d = yv ? yv[I.ei[k]] * yv[I.ej[k]] : 0.0;
+        const double bk = I.b_up ? I.b_up[k] : 0.0;
+        const double t = (P.r_up[k] + bk) - d;
+        v[1] = v[1] + t * t;
+      }
+      team_sum<2>(c.t, c.rs, v);
+      double sq = v[1];
+      if (is_theta(I)) {
+        const double t = (rt + I.b_trace) - v[0];
+        sq = sq + t * t;
+      }
+      denom = beta * sq;
+    }
+    const double numer = gap;
+    double alpha;
+    if (denom <= 1e-14)
+      alpha = numer > 0 ? 1.0 : 0.0;
+    else
+      alpha = fmin(fmax(numer / denom, 0.0), 1.0);
+    int s_new = s;
+    if (theta > 0 && alpha != 1.0 && s + 1 > kSMax) {
+      fail(c, kErrCapacity, kMsgRankCap);
+      return false;
+    }
+    {
+      double* dst = P.buf[R.tmp];
+      HALLAR_DISPATCH_S(s, rank_update_dev<S_>(c, P, Y, s, yv, alpha, theta > 0, dst, &s_new));
+      const int t = R.yt;
+      R.yt = R.tmp;
+      R.tmp = t;
+    }
+    s = s_new;
+    ++out.fw_steps;
+    if (cf.trace) {
+      double al;
+      HALLAR_DISPATCH_S(s, ok = al_value_dev<S_>(c, P, P.buf[R.yt], s, P.p_up, c.p_trace, beta,
+                                                 &al, nullptr));
+      if (!ok) return false;
+      TraceEv ev{};
+      ev.kind = 1;
+      ev.outer_iter = outer_iter;
+      ev.beta = beta;
+      ev.eps_inner = eps_t;
+      ev.gap = gap;
+      ev.theta = theta;
+      ev.rank = s;
+      ev.fw_alpha = alpha;
+      ev.al_value = al;
+      emit_trace(P, c, ev);
+    }
+  }
+}
+
+}  // namespace hallar

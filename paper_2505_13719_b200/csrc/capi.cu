@@ -159,7 +159,8 @@ struct cuhallar_instance {
   // device arrays
   int32_t *ei = nullptr, *ej = nullptr, *lo_col = nullptr;
   int64_t *up_ptr = nullptr, *lo_ptr = nullptr, *lo_eid = nullptr;
-  double *b_up = nullptr, *b_lo = nullptr;
+  double *b_up = nullptr, *b_lo = nullptr;      // scaled b/tau (solve)
+  double *ub_up = nullptr, *ub_lo = nullptr;    // unscaled b (operator ABI), lazy
   // workspace
   int ws_grid = 0;
   unsigned long long* bar = nullptr;
@@ -184,7 +185,7 @@ struct cuhallar_instance {
     auto f = [](void* p) {
       if (p) cudaFree(p);
     };
-    f(ei); f(ej); f(lo_col); f(up_ptr); f(lo_ptr); f(lo_eid); f(b_up); f(b_lo);
+    f(ei); f(ej); f(lo_col); f(up_ptr); f(lo_ptr); f(lo_eid); f(b_up); f(b_lo); f(ub_up); f(ub_lo);
     f(bar); f(slots); for (auto* b : buf) f(b); f(vslot);
     f(p_up); f(p_lo); f(q_up); f(q_lo); f(r_up); f(r_lo); f(lz_rand); f(dscal); f(discal); f(dso);
     if (trace_host) cudaFreeHost(trace_host);
@@ -403,6 +404,21 @@ Params base_params(cuhallar_instance* in, const cuhallar_config* cfg) {
     P.trace_cap = in->trace_cap;
   }
   return P;
+}
+
+// Operator calls act on the instance as built (unscaled b), like the
+// reference's al_value(inst, ...) / GradientOperator(inst, ...); only the
+// solve works on the scaled instance b / tau (solver.cpp:31-42).
+void use_unscaled_b(cuhallar_instance* in, Params& P) {
+  if (in->h.has_trace || in->h.tau == 1.0) return;
+  if (!in->ub_up) {
+    std::vector<double> up(in->h.b.begin(), in->h.b.begin() + in->h.np), lo(in->h.np);
+    for (int64_t e = 0; e < in->h.np; ++e) lo[e] = up[in->lo_eid_host[e]];
+    in->ub_up = dupload(up, &in->bytes);
+    in->ub_lo = dupload(lo, &in->bytes);
+  }
+  P.I.b_up = in->ub_up;
+  P.I.b_lo = in->ub_lo;
 }
 
 // Launch the persistent kernel; returns the solver status and fills *so.
@@ -633,6 +649,7 @@ static int run_op(cuhallar_instance* in, int op, const double* U_dev, int64_t ld
     P.op = op;
     P.s_in = s;
     P.beta_in = beta;
+    use_unscaled_b(in, P);
     load_factor_dev(in, U_dev, ldu, s, st);
     if (op == kOpCPlusAdj || op == kOpAdj) {
       P.q_trace_in = load_multiplier_dev(in, vec_dev, in->q_up, in->q_lo, st);
@@ -834,6 +851,7 @@ int cuhallar_min_eig_gradient(cuhallar_instance* in, const double* U_host, int s
     cfg.eig_block_restart = block_restart;
     Params P = base_params(in, &cfg);
     P.op = kOpMinEigG;
+    use_unscaled_b(in, P);
     P.s_in = s;
     P.beta_in = beta;
     P.rho_in = tol;
@@ -869,6 +887,7 @@ int cuhallar_aipp(cuhallar_instance* in, const double* p_host, double beta, cons
     ensure_workspace(in, grid, 0, 30);
     Params P = base_params(in, cfg);
     P.op = kOpAipp;
+    use_unscaled_b(in, P);
     P.s_in = s;
     P.beta_in = beta;
     P.rho_in = rho;

@@ -112,7 +112,6 @@ __device__ __noinline__ void solve_dev(Ctx& c, const Params& P, SolveOut* so) {
   double prev_pfeas = INFINITY;
   int status = 1;  // iteration limit
   bool nan_report = false;
-  bool numerical = false;
 
   for (int t = 1; t <= cf.max_outer; ++t) {
     if (team_now(c) >= deadline) {
@@ -126,7 +125,6 @@ __device__ __noinline__ void solve_dev(Ctx& c, const Params& P, SolveOut* so) {
     HlrOut ho;
     if (!hlr_dev(c, P, R, s, beta, eps_t, t, (unsigned long long)deadline, ho)) {
       if (c.status == kErrNumerical) {
-        numerical = true;
         c.status = kOk;  // caught: finish(kNumericalFailure)
         status = 3;
         o.outer_iters = o.outer_iters;  // unchanged
@@ -234,7 +232,6 @@ __device__ __noinline__ void solve_dev(Ctx& c, const Params& P, SolveOut* so) {
     }
     return;
   }
-  (void)numerical;
   // finish() (solver.cpp:175-202)
   if (!have_cert && !nan_report) {
     Cert ct;

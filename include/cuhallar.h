@@ -80,6 +80,8 @@ typedef struct {
   double tau, norm_b1, norm_C1;
   double nuclear_norm; /* matcomp only */
   int64_t device_bytes; /* HBM held by the instance */
+  int64_t h2d_bytes;    /* host->device bytes copied so far (upload + solves) */
+  int team_ctas;        /* persistent CTAs per launch on this device */
 } cuhallar_instance_info;
 /* SdpInstance public fields  sdp_instance.hpp:22-35 */
 int cuhallar_instance_get_info(const cuhallar_instance* inst, cuhallar_instance_info* out);
@@ -192,6 +194,16 @@ int cuhallar_aipp(cuhallar_instance* inst, const double* p_host, double beta,
                   const double* W_host, int s, double rho, const cuhallar_config* cfg,
                   double* W_out_host, int* status, int* prox_iters, int* fista_iters,
                   double* R_norm, double* g_value, double* lambda);
+
+/* ------------------------------------------------------ measurement ------ */
+/* In-kernel timing of one solver pass repeated `iters` times inside a single
+ * persistent launch: kind 0 team barrier, 1 team all-reduce (5 values),
+ * 2 fused value+gradient row pass (C + A*(p + beta(A(UU')-b)))U + reductions,
+ * 3 constraint map pass A(UU') + reductions, 4 Lanczos matvec (fixed q, s=1).
+ * U_host n x s column-major, p_host length m.  *ns_per_pass from %globaltimer. */
+int cuhallar_bench_pass(cuhallar_instance* inst, int kind, const double* U_host, int s,
+                        const double* p_host, double beta, int iters, int team_ctas,
+                        double* ns_per_pass);
 
 #ifdef __cplusplus
 }

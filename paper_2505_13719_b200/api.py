@@ -99,7 +99,7 @@ class CInfo(C.Structure):
         ("n", C.c_int64), ("m", C.c_int64), ("identity_constraint", C.c_int64),
         ("field_kind", C.c_int), ("family", C.c_int), ("tau", C.c_double),
         ("norm_b1", C.c_double), ("norm_C1", C.c_double), ("nuclear_norm", C.c_double),
-        ("device_bytes", C.c_int64),
+        ("device_bytes", C.c_int64), ("h2d_bytes", C.c_int64), ("team_ctas", C.c_int),
     ]
 
 
@@ -175,6 +175,11 @@ class SdpInstance:
         self.norm_C1 = float(info.norm_C1)
         self.nuclear_norm = float(info.nuclear_norm)
         self.device_bytes = int(info.device_bytes)
+
+    def info(self) -> dict:
+        i = CInfo()
+        _check(_lib.cuhallar_instance_get_info(self._h, C.byref(i)))
+        return {k: getattr(i, k) for k, _ in CInfo._fields_}
 
     def __del__(self):
         try:
@@ -298,6 +303,18 @@ class SdpInstance:
             C.c_double(tol), C.c_int(max_iters), C.c_int(block_restart), C.c_uint64(seed), C.byref(lam),
             v.ctypes.data_as(_dp), C.byref(res), C.byref(mv), C.byref(conv)))
         return dict(lambda_=lam.value, v=v, residual=res.value, matvecs=mv.value, converged=bool(conv.value))
+
+    BENCH_KINDS = {"sync": 0, "allreduce": 1, "grad_pass": 2, "map_pass": 3, "lanczos_matvec": 4}
+
+    def bench_pass(self, kind, U, p, beta=1.0, iters=100, team_ctas=0) -> float:
+        """ns per pass of one solver phase, timed inside a persistent launch."""
+        U = np.asfortranarray(np.asarray(U, dtype=np.float64).reshape(self.n, -1))
+        p = np.ascontiguousarray(p, dtype=np.float64)
+        ns = C.c_double()
+        _check(_lib.cuhallar_bench_pass(self._h, C.c_int(self.BENCH_KINDS.get(kind, kind)),
+                                        U.ctypes.data_as(_dp), C.c_int(U.shape[1]), p.ctypes.data_as(_dp),
+                                        C.c_double(beta), C.c_int(iters), C.c_int(team_ctas), C.byref(ns)))
+        return ns.value
 
     def aipp(self, p, beta, W, rho, cfg: "SolverConfig" = None):
         W = np.asfortranarray(np.asarray(W, dtype=np.float64).reshape(self.n, -1))

@@ -155,6 +155,7 @@ struct cuhallar_instance {
   hh::HostInst h;
   DevPairs I{};
   int64_t bytes = 0;
+  int64_t h2d = 0;
   std::vector<int64_t> lo_eid_host;
   // device arrays
   int32_t *ei = nullptr, *ej = nullptr, *lo_col = nullptr;
@@ -232,6 +233,7 @@ void upload_pairs(cuhallar_instance* in) {
   in->lo_col = dupload(lo_col, &in->bytes);
   in->lo_eid = dupload(lo_eid, &in->bytes);
   in->lo_eid_host = std::move(lo_eid);
+  in->h2d += in->bytes;
   DevPairs& I = in->I;
   I.family = h.family;
   I.has_trace = h.has_trace ? 1 : 0;
@@ -261,6 +263,7 @@ void upload_pairs(cuhallar_instance* in) {
     bs.resize(np);
     in->b_up = dupload(bs, &in->bytes);
     in->b_lo = dupload(bl, &in->bytes);
+    in->h2d += int64_t(2 * np * sizeof(double));
     I.b_up = in->b_up;
     I.b_lo = in->b_lo;
   }
@@ -303,6 +306,7 @@ void ensure_workspace(cuhallar_instance* in, int grid, uint64_t seed, int block_
     const auto v = hh::gaussian_stream(seed ^ 0x9b97f4a7c15ULL, n * (1 + refill));
     if (in->lz_rand) cudaFree(in->lz_rand);
     in->lz_rand = dupload(v, &in->bytes);
+    in->h2d += int64_t(v.size() * sizeof(double));
     in->n_refill = refill;
     in->lz_seed = seed;
   }
@@ -617,6 +621,12 @@ int cuhallar_instance_get_info(const cuhallar_instance* in, cuhallar_instance_in
   o->norm_C1 = in->h.norm_C1;
   o->nuclear_norm = in->h.nuclear;
   o->device_bytes = in->bytes;
+  o->h2d_bytes = in->h2d;
+  o->team_ctas = 0;
+  try {
+    o->team_ctas = grid_size(0);
+  } catch (...) {
+  }
   return 0;
 }
 int cuhallar_instance_get_b(const cuhallar_instance* in, double* b) {
@@ -721,6 +731,7 @@ static void host_factor_to_buf0(cuhallar_instance* in, const double* U_host, int
   for (int64_t a = 0; a < n; ++a)
     for (int k = 0; k < s; ++k) rm[a * s + k] = U_host[a + k * n];
   ck(cudaMemcpy(in->buf[0], rm.data(), rm.size() * sizeof(double), cudaMemcpyHostToDevice), "U0");
+  in->h2d += int64_t(rm.size() * sizeof(double));
 }
 static double host_multiplier_to_dev(cuhallar_instance* in, const double* p_host) {
   const int64_t np = in->h.np;
@@ -729,6 +740,7 @@ static double host_multiplier_to_dev(cuhallar_instance* in, const double* p_host
   for (int64_t e = 0; e < np; ++e) lo[e] = up[in->lo_eid_host[e]];
   ck(cudaMemcpy(in->p_up, up.data(), np * sizeof(double), cudaMemcpyHostToDevice), "p_up");
   ck(cudaMemcpy(in->p_lo, lo.data(), np * sizeof(double), cudaMemcpyHostToDevice), "p_lo");
+  in->h2d += int64_t(2 * np * sizeof(double));
   return (in->h.has_trace && p_host) ? p_host[np] : 0.0;
 }
 
@@ -758,6 +770,7 @@ int cuhallar_solve(cuhallar_instance* in, const cuhallar_config* cfg, const doub
       const double nu = std::sqrt(hh::eigen_order_sum_sq(u0.data(), n));
       for (auto& x : u0) x = x / nu;
       ck(cudaMemcpy(in->buf[0], u0.data(), n * sizeof(double), cudaMemcpyHostToDevice), "U0");
+      in->h2d += int64_t(n * sizeof(double));
     }
     Params P = base_params(in, cfg);
     P.op = kOpSolve;
@@ -912,6 +925,32 @@ int cuhallar_aipp(cuhallar_instance* in, const double* p_host, double beta, cons
     ck(cudaMemcpy(rm.data(), wout, rm.size() * sizeof(double), cudaMemcpyDeviceToHost), "W");
     for (int64_t a = 0; a < in->h.n; ++a)
       for (int k = 0; k < s; ++k) W_out[a + k * in->h.n] = rm[a * s + k];
+    return 0;
+  });
+}
+
+int cuhallar_bench_pass(cuhallar_instance* in, int kind, const double* U_host, int s,
+                        const double* p_host, double beta, int iters, int team_ctas,
+                        double* ns_per_pass) {
+  return guard([&] {
+    check_pairs(in);
+    if (s < 1 || s > kSMax) throw hh::InputError("factor rank must be in [1, 32]");
+    std::lock_guard<std::mutex> lk(in->mu);
+    const int grid = grid_size(team_ctas);
+    ensure_workspace(in, grid, 0, 30);
+    Params P = base_params(in, nullptr);
+    P.op = kOpBench;
+    P.bench_kind = kind;
+    P.bench_iters = iters;
+    P.s_in = s;
+    P.beta_in = beta;
+    host_factor_to_buf0(in, U_host, s);
+    P.p_trace = host_multiplier_to_dev(in, p_host);
+    P.out_mat = in->buf[11];
+    SolveOut so{};
+    const int stt = launch(in, P, grid, 0, &so);
+    if (stt != kOk) return status_to_rc(stt, so.msg);
+    ck(cudaMemcpy(ns_per_pass, in->dscal, sizeof(double), cudaMemcpyDeviceToHost), "ns");
     return 0;
   });
 }

@@ -81,6 +81,7 @@ enum Op : int {
   kOpAlGrad = 7,       // out = gradient
   kOpMinEigG = 8,      // Lanczos on G(U,p,beta)
   kOpAipp = 9,         // aipp on L_beta(.;p) from U
+  kOpBench = 10,       // repeat one pass bench_iters times, scalars[0] = ns / pass
 };
 
 // Everything the persistent kernel touches; lives in device memory.
@@ -112,6 +113,8 @@ struct Params {
   double beta_in = 0.0;
   double q_trace_in = 0.0;   // kOpCPlusAdj / kOpAdj: q[m-1]
   double rho_in = 0.0;
+  int bench_kind = 0;
+  int bench_iters = 0;
   double* out_vec = nullptr; // kOpMap
   double* out_mat = nullptr; // row-major n x s
   // outputs

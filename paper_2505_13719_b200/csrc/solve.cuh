@@ -396,6 +396,69 @@ __device__ __noinline__ void op_dispatch(Ctx& c, const Params& P, SolveOut* so) 
       }
       break;
     }
+    case kOpBench: {
+      // In-kernel pass timing (CTA 0's globaltimer around bench_iters passes).
+      double nrm2;
+      factor_stats<S>(c, P, U, s, &nrm2);
+      const double beta = P.beta_in;
+      double rt = 0.0, qt = 0.0;
+      if (is_theta(I)) {
+        rt = nrm2 - I.b_trace;
+        qt = P.p_trace + beta * rt;
+      }
+      double* out = P.out_mat;
+      c.t.sync();
+      const unsigned long long t0 = globaltimer_ns();
+      for (int it = 0; it < P.bench_iters; ++it) {
+        switch (P.bench_kind) {
+          case 0:
+            c.t.sync();
+            break;
+          case 1: {
+            double v[5] = {1.0, 2.0, 3.0, 4.0, 5.0};
+            team_sum<5>(c.t, c.rs, v);
+            break;
+          }
+          case 2: {  // fused value + gradient row pass (FISTA T2 / T5 shape)
+            double hU = 0.0;
+            auto epi = [&](int64_t a, double h, double uo) {
+              if (c.lane < s) {
+                hU = hU + h * uo;
+                out[a * s + c.lane] = 2.0 * h;
+              }
+            };
+            double sums[3] = {0, 0, 0};
+            row_pass<S, false>(c, P, U, s, P.p_up, P.p_lo, beta, theta_alpha_or_half(I, qt),
+                               is_theta(I) ? c.cs : nullptr, false, sums, epi);
+            double v[4] = {hU, sums[0], sums[1], sums[2]};
+            team_sum<4>(c.t, c.rs, v);
+            break;
+          }
+          case 3: {  // map pass (FISTA T4 shape)
+            double ms[2] = {0.0, 0.0};
+            map_pass<S>(c, P, U, s, kMapPR, P.p_up, nullptr, nullptr, ms);
+            team_sum<2>(c.t, c.rs, ms);
+            break;
+          }
+          case 4: {  // Lanczos matvec: fixed-q adjoint at s = 1 on column 0
+            auto epi = [&](int64_t a, double h, double) {
+              if (c.lane == 0) out[a] = -h;
+            };
+            double sums[3] = {0, 0, 0};
+            row_pass<1, true>(c, P, U, 1, P.p_up, P.p_lo, 0.0, theta_alpha_or_half(I, qt),
+                              is_theta(I) ? c.cs : nullptr, false, sums, epi);
+            c.t.sync();
+            break;
+          }
+          default:
+            break;
+        }
+      }
+      c.t.sync();
+      if (c.t.rank == 0 && threadIdx.x == 0)
+        P.scalars[0] = (double)(globaltimer_ns() - t0) / (double)max(1, P.bench_iters);
+      break;
+    }
     default:
       break;
   }

@@ -140,6 +140,7 @@ typedef struct {
   int threads;   /* record-only, as in the reference (README.md:108-111) */
   int trace;     /* deliver TraceEvents to the callback (costs one extra map per rank step) */
   int team_ctas; /* 0 = one persistent CTA per SM slot (auto) */
+  int profile;   /* record per-phase device time (cuhallar_last_profile) */
 } cuhallar_config;
 /* Fills the reference defaults. */
 void cuhallar_config_default(cuhallar_config* cfg);
@@ -204,6 +205,13 @@ int cuhallar_aipp(cuhallar_instance* inst, const double* p_host, double beta,
 int cuhallar_bench_pass(cuhallar_instance* inst, int kind, const double* U_host, int s,
                         const double* p_host, double beta, int iters, int team_ctas,
                         double* ns_per_pass);
+
+/* Per-phase device time of the last profiled solve (cfg.profile = 1):
+ * categories 0 fista_x~, 1 fista_value_grad, 2 fista_y+_map, 3 fista_grad_y+,
+ * 4 aipp, 5 lanczos_apply, 6 lanczos_cgs2, 7 jacobi, 8 lanczos_measure,
+ * 9 lanczos_restart, 10 gradient_operator, 11 fw_gap, 12 fw_step, 13 outer, 14 other.
+ * Returns the number of categories written (0 if none recorded). */
+int cuhallar_last_profile(const cuhallar_instance* inst, double* ns, int64_t* counts, int cap);
 
 #ifdef __cplusplus
 }

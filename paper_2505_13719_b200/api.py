@@ -78,7 +78,7 @@ class CConfig(C.Structure):
         ("aipp_lambda_underflow", C.c_double), ("fista_sigma", C.c_double),
         ("fista_chi", C.c_double), ("fista_mu", C.c_double), ("fista_L0", C.c_double),
         ("fista_max_iters", C.c_int), ("max_fw_steps", C.c_int), ("threads", C.c_int),
-        ("trace", C.c_int), ("team_ctas", C.c_int),
+        ("trace", C.c_int), ("team_ctas", C.c_int), ("profile", C.c_int),
     ]
 
 
@@ -304,6 +304,16 @@ class SdpInstance:
             v.ctypes.data_as(_dp), C.byref(res), C.byref(mv), C.byref(conv)))
         return dict(lambda_=lam.value, v=v, residual=res.value, matvecs=mv.value, converged=bool(conv.value))
 
+    PROFILE_CATS = ["fista_x~", "fista_value_grad", "fista_y+_map", "fista_grad_y+", "aipp",
+                    "lanczos_apply", "lanczos_cgs2", "jacobi", "lanczos_measure", "lanczos_restart",
+                    "gradient_operator", "fw_gap", "fw_step", "outer", "other"]
+
+    def last_profile(self) -> dict:
+        ns = (C.c_double * 16)()
+        cnt = (C.c_int64 * 16)()
+        k = _lib.cuhallar_last_profile(self._h, ns, cnt, 16)
+        return {self.PROFILE_CATS[i]: (ns[i] * 1e-6, int(cnt[i])) for i in range(min(k, len(self.PROFILE_CATS)))}
+
     BENCH_KINDS = {"sync": 0, "allreduce": 1, "grad_pass": 2, "map_pass": 3, "lanczos_matvec": 4}
 
     def bench_pass(self, kind, U, p, beta=1.0, iters=100, team_ctas=0) -> float:
@@ -423,12 +433,15 @@ class SolverConfig:
     deterministic: bool = False
     threads: int = 0
     team_ctas: int = 0
+    profile: bool = False
 
     def _c(self, trace=False) -> CConfig:
         c = CConfig()
         for name, _ in CConfig._fields_:
             if name == "trace":
                 c.trace = 1 if trace else 0
+            elif name == "profile":
+                c.profile = 1 if self.profile else 0
             else:
                 setattr(c, name, getattr(self, name))
         return c

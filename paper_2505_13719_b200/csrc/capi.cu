@@ -41,7 +41,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   c.tile = sm + c.warp * kTile * kTileLd;
   sm += kWarps * kTile * kTileLd;
   c.cs = sm;
-  sm += kSMax;
+  sm += 2 * kSMax;
   c.H = sm;
   sm += kHLd * kHLd;
   c.JA = sm;
@@ -103,7 +103,7 @@ namespace {
 thread_local std::string g_err;
 
 constexpr size_t kSmemBytes =
-    sizeof(double) * (kWarps * kRedK + kRedK + kWarps * kTile * kTileLd + kSMax + kHLd * kHLd +
+    sizeof(double) * (kWarps * kRedK + kRedK + kWarps * kTile * kTileLd + 2 * kSMax + kHLd * kHLd +
                       3 * 32 * 32 + 4 * 32 + 64) +
     sizeof(int) * 80;
 
@@ -142,7 +142,7 @@ int grid_size(int requested) {
     ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, hallar_kernel, kThreads, kSmemBytes),
        "occupancy");
     if (per < 1) throw CudaError("hallar_kernel cannot be resident");
-    cached = sms * per;
+    cached = std::min(sms * per, kMaxTeam);
   }
   if (requested > 0) return std::min(requested, cached);
   return cached;
@@ -177,6 +177,8 @@ struct cuhallar_instance {
   double* dscal = nullptr;
   int* discal = nullptr;
   SolveOut* dso = nullptr;
+  unsigned long long* dprof = nullptr;
+  std::vector<unsigned long long> last_prof;
   TraceEv* trace_host = nullptr;
   int* trace_count_host = nullptr;
   int trace_cap = 4096;
@@ -188,7 +190,7 @@ struct cuhallar_instance {
     };
     f(ei); f(ej); f(lo_col); f(up_ptr); f(lo_ptr); f(lo_eid); f(b_up); f(b_lo); f(ub_up); f(ub_lo);
     f(bar); f(slots); for (auto* b : buf) f(b); f(vslot);
-    f(p_up); f(p_lo); f(q_up); f(q_lo); f(r_up); f(r_lo); f(lz_rand); f(dscal); f(discal); f(dso);
+    f(p_up); f(p_lo); f(q_up); f(q_lo); f(r_up); f(r_lo); f(lz_rand); f(dscal); f(discal); f(dso); f(dprof);
     if (trace_host) cudaFreeHost(trace_host);
     if (trace_count_host) cudaFreeHost(trace_count_host);
   }
@@ -776,9 +778,20 @@ int cuhallar_solve(cuhallar_instance* in, const cuhallar_config* cfg, const doub
     P.op = kOpSolve;
     P.s_in = s;
     P.p_trace = host_multiplier_to_dev(in, p0_host);
+    if (cfg->profile) {
+      if (!in->dprof) in->dprof = dalloc<unsigned long long>(2 * kProfCats, &in->bytes);
+      ck(cudaMemset(in->dprof, 0, sizeof(unsigned long long) * 2 * kProfCats), "prof");
+      P.prof = in->dprof;
+    }
     SolveOut so{};
     float ms = 0.f;
     const int stt = launch(in, P, grid, 0, &so, &ms);
+    if (cfg->profile) {
+      in->last_prof.assign(2 * kProfCats, 0);
+      ck(cudaMemcpy(in->last_prof.data(), in->dprof, sizeof(unsigned long long) * 2 * kProfCats,
+                    cudaMemcpyDeviceToHost),
+         "prof D2H");
+    }
     const double wall =
         std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();
     if (fn && cfg->trace) {
@@ -834,6 +847,16 @@ int cuhallar_solve(cuhallar_instance* in, const cuhallar_config* cfg, const doub
     }
     return 0;
   });
+}
+
+int cuhallar_last_profile(const cuhallar_instance* in, double* ns, int64_t* counts, int cap) {
+  if (in->last_prof.empty()) return 0;
+  const int k = std::min<int>(cap, kProfCats);
+  for (int i = 0; i < k; ++i) {
+    ns[i] = double(in->last_prof[i]);
+    counts[i] = int64_t(in->last_prof[kProfCats + i]);
+  }
+  return k;
 }
 
 int cuhallar_solution_get_U(const cuhallar_solution* s, double* U) {

@@ -12,8 +12,15 @@ constexpr int kLanczosMax = 32;          // max Lanczos basis (block_restart cap
 constexpr int kRedK = 40;                // max values per team reduction
 constexpr int kNBuf = 12;                // n x kSMax factor buffers in the pool
 constexpr int kTile = 8;                 // columns per fold chunk
+constexpr int kMaxTeam = 320;            // max persistent CTAs (team reduction width)
 
 enum Family : int { kTheta = 0, kMatcomp = 1, kPhaseret = 2 };
+
+// Optional in-solve phase profile (CTA 0's %globaltimer between phase ends).
+enum ProfCat : int {
+  kPfT1 = 0, kPfT2, kPfT34, kPfT5, kPfAipp, kPfLzApply, kPfLzCgs, kPfJacobi, kPfLzMeasure,
+  kPfLzRestart, kPfGradop, kPfGap, kPfFwStep, kPfOuter, kPfOther, kProfCats
+};
 
 enum Status : int {
   kOk = 0,
@@ -114,6 +121,7 @@ struct Params {
   double q_trace_in = 0.0;   // kOpCPlusAdj / kOpAdj: q[m-1]
   double rho_in = 0.0;
   int bench_kind = 0;
+  unsigned long long* prof = nullptr;  // [2 * kProfCats]: ns, count
   int bench_iters = 0;
   double* out_vec = nullptr; // kOpMap
   double* out_mat = nullptr; // row-major n x s

@@ -55,11 +55,26 @@ struct Ctx {
   int warp, lane;
   int status = kOk;
   int msg = kMsgNone;
+  unsigned long long prof_last = 0;
   double beta = 0.0;     // current AL penalty (replicated)
   double p_trace = 0.0;  // current p[m-1] (theta trace multiplier)
 };
 
 __device__ __forceinline__ bool is_theta(const DevPairs& I) { return I.has_trace != 0; }
+
+__device__ __forceinline__ unsigned long long gtimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ void prof_mark(Ctx& c, const Params& P, int cat) {
+  if (P.prof && c.t.rank == 0 && threadIdx.x == 0) {
+    const unsigned long long now = gtimer_ns();
+    P.prof[cat] += now - c.prof_last;
+    P.prof[kProfCats + cat] += 1;
+    c.prof_last = now;
+  }
+}
 
 __device__ __forceinline__ void fail(Ctx& c, int status, int msg) {
   if (c.status == kOk) {
@@ -96,7 +111,7 @@ __device__ int64_t row_split(const DevPairs& I, int rank, int size) {
 //   sums[0] += p r, sums[1] += r^2, sums[2] += q (r + b).
 // epi(a, h, u_own) is called warp-uniformly; lanes >= s carry junk.
 template <int S, bool FIXED, class Epi>
-__device__ __noinline__ void row_pass(Ctx& c, const Params& P, const double* __restrict__ U, int s_rt,
+__device__ __forceinline__ void row_pass(Ctx& c, const Params& P, const double* __restrict__ U, int s_rt,
                          const double* __restrict__ Pup, const double* __restrict__ Plo,
                          double beta, double alpha, const double* cs, bool zero_init,
                          double (&sums)[3], Epi& epi) {
@@ -187,7 +202,7 @@ __device__ __noinline__ void row_pass(Ctx& c, const Params& P, const double* __r
 // r_k = U_a.U_b - b_k and q_k = p_k + beta r_k, written in edge order (upper
 // entries) and lower order.  Upper entries accumulate p.r and r^2.
 template <int S>
-__device__ __noinline__ void gradop_pass(Ctx& c, const Params& P, const double* __restrict__ U, int s_rt,
+__device__ __forceinline__ void gradop_pass(Ctx& c, const Params& P, const double* __restrict__ U, int s_rt,
                             double beta, double (&sums)[2], bool* nonfinite) {
   const DevPairs& I = P.I;
   constexpr int SR = S > 0 ? S : kSMax;
@@ -242,74 +257,171 @@ __device__ __noinline__ void gradop_pass(Ctx& c, const Params& P, const double* 
 
 // ------------------------------------------------------------- map pass ---
 // Thread per pair constraint k (edge order): d_k = U_{i_k}.U_{j_k} summed over
-// columns in order (instances.cpp:27-35).
+// columns in order (instances.cpp:27-35).  kUnroll constraints per thread are
+// loaded before any is used so each thread keeps several gathers in flight.
 enum MapMode : int { kMapPR = 0, kMapRR = 1, kMapOut = 2, kMapFWS = 3 };
+constexpr int kUnroll = 4;
+
+// Row values of the gathered factor: either stored (U) or produced on the fly
+// from the FISTA step y = (xt - gt/L) [/ nrm] (bit-identical to storing y).
+struct RowSrc {
+  const double* U = nullptr;
+  const double* XT = nullptr;
+  const double* GT = nullptr;
+  double L = 1.0, nrm = 1.0;
+  bool scale = false;
+  __device__ __forceinline__ double at(int64_t o) const {
+    if (U) return U[o];
+    const double z = XT[o] - GT[o] / L;
+    return scale ? z / nrm : z;
+  }
+};
+
 template <int S>
-__device__ __noinline__ void map_pass(Ctx& c, const Params& P, const double* __restrict__ U, int s_rt,
-                         int mode, const double* __restrict__ pup, double* out,
-                         const double* __restrict__ ref, double (&sums)[2]) {
+__device__ __forceinline__ void map_pass_src(Ctx& c, const Params& P, const RowSrc src, int s_rt,
+                                          int mode, const double* __restrict__ pup, double* out,
+                                          const double* __restrict__ ref, double (&sums)[2]) {
   const DevPairs& I = P.I;
-  constexpr int SR = S > 0 ? S : kSMax;
   const int s = S > 0 ? S : s_rt;
-  for (int64_t k = c.kl + threadIdx.x; k < c.kh; k += kThreads) {
-    const int64_t i = I.ei[k], j = I.ej[k];
-    double d = 0.0;
+  for (int64_t k0 = c.kl + threadIdx.x; k0 < c.kh; k0 += (int64_t)kThreads * kUnroll) {
+    int64_t ii[kUnroll], jj[kUnroll];
+    double pk[kUnroll], bk[kUnroll], rf[kUnroll];
 #pragma unroll
-    for (int cc = 0; cc < SR; ++cc)
-      if (cc < s) {
-        const double t = U[i * s + cc] * U[j * s + cc];
-        d = (cc == 0) ? t : d + t;
+    for (int u = 0; u < kUnroll; ++u) {
+      const int64_t k = k0 + (int64_t)u * kThreads;
+      const bool ok = k < c.kh;
+      ii[u] = ok ? I.ei[k] : 0;
+      jj[u] = ok ? I.ej[k] : 0;
+      bk[u] = (ok && I.b_up) ? I.b_up[k] : 0.0;
+      pk[u] = (ok && mode == kMapPR) ? pup[k] : 0.0;
+      rf[u] = (ok && mode == kMapFWS) ? ref[k] : 0.0;
+    }
+    double d[kUnroll];
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      double acc = 0.0;
+      if (S > 0) {
+#pragma unroll
+        for (int cc = 0; cc < (S > 0 ? S : 1); ++cc) {
+          const double t = src.at(ii[u] * s + cc) * src.at(jj[u] * s + cc);
+          acc = (cc == 0) ? t : acc + t;
+        }
+      } else {
+        for (int cc = 0; cc < s; ++cc) {
+          const double t = src.at(ii[u] * s + cc) * src.at(jj[u] * s + cc);
+          acc = (cc == 0) ? t : acc + t;
+        }
       }
-    const double bk = I.b_up ? I.b_up[k] : 0.0;
-    if (mode == kMapOut) {
-      out[k] = d;
-    } else if (mode == kMapFWS) {
-      const double t = (ref[k] + bk) - d;
-      sums[1] = sums[1] + t * t;
-    } else {
-      const double r = d - bk;
-      if (mode == kMapPR) sums[0] = sums[0] + pup[k] * r;
-      sums[1] = sums[1] + r * r;
+      d[u] = acc;
+    }
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      const int64_t k = k0 + (int64_t)u * kThreads;
+      if (k >= c.kh) continue;
+      if (mode == kMapOut) {
+        out[k] = d[u];
+      } else if (mode == kMapFWS) {
+        const double t = (rf[u] + bk[u]) - d[u];
+        sums[1] = sums[1] + t * t;
+      } else {
+        const double r = d[u] - bk[u];
+        if (mode == kMapPR) sums[0] = sums[0] + pk[u] * r;
+        sums[1] = sums[1] + r * r;
+      }
     }
   }
 }
 
-// -------------------------------------------------------- factor helpers ---
-// Statistics of a factor needed before gathering it: theta needs ||U||_F^2
-// (trace constraint) and the column sums (C = -ee'); MC needs 0.5||U||^2.
-// On return (all CTAs): nrm2, and c.cs[0..s) filled for theta.
 template <int S>
-__device__ __noinline__ void factor_stats(Ctx& c, const Params& P, const double* __restrict__ U, int s_rt,
-                             double* nrm2) {
-  constexpr int SR = S > 0 ? S : kSMax;
+__device__ __forceinline__ void map_pass(Ctx& c, const Params& P, const double* __restrict__ U,
+                                         int s_rt, int mode, const double* __restrict__ pup,
+                                         double* out, const double* __restrict__ ref,
+                                         double (&sums)[2]) {
+  RowSrc src;
+  src.U = U;
+  map_pass_src<S>(c, P, src, s_rt, mode, pup, out, ref, sums);
+}
+
+// -------------------------------------------------------- factor helpers ---
+// Per-row loop over this CTA's rows with column statistics.  For S > 0 a
+// thread owns whole rows (S column accumulators in registers); for the
+// generic rank (S == 0) a warp owns a row and lane c owns column c, so the
+// column accumulator is one register per lane.  f(o, k) returns the element
+// value at offset o = a*s + k; colsum partials are staged into the reduction
+// smem at [base, base + s).
+template <int S, class F>
+__device__ __forceinline__ void rows_colsum(Ctx& c, int s_rt, int base, F&& f) {
   const int s = S > 0 ? S : s_rt;
-  double v[SR + 1];
+  if constexpr (S > 0) {
+    double cs[S];
 #pragma unroll
-  for (int k = 0; k <= SR; ++k) v[k] = 0.0;
-  for (int64_t a = c.rl + threadIdx.x; a < c.rh; a += kThreads) {
+    for (int k = 0; k < S; ++k) cs[k] = 0.0;
+    for (int64_t a = c.rl + threadIdx.x; a < c.rh; a += kThreads) {
 #pragma unroll
-    for (int k = 0; k < SR; ++k)
-      if (k < s) {
-        const double u = U[a * s + k];
-        v[0] = v[0] + u * u;
-        v[1 + k] = v[1 + k] + u;
-      }
+      for (int k = 0; k < S; ++k) cs[k] = cs[k] + f(a * S + k, k);
+    }
+#pragma unroll
+    for (int k = 0; k < S; ++k) {
+      const double x = warp_sum(cs[k]);
+      if (c.lane == 0) c.rs.part[c.warp * kRedK + base + k] = x;
+    }
+  } else {
+    double cs = 0.0;
+    for (int64_t a = c.rl + c.warp; a < c.rh; a += kWarps)
+      if (c.lane < s) cs = cs + f(a * s + c.lane, c.lane);
+    if (c.lane < s) c.rs.part[c.warp * kRedK + base + c.lane] = cs;
   }
-  team_sum<SR + 1>(c.t, c.rs, v);
-  *nrm2 = v[0];
-  if (threadIdx.x < (unsigned)s) c.cs[threadIdx.x] = c.rs.out[1 + threadIdx.x];
+}
+
+// Stage NV per-thread scalars (warp-summed) at [0, NV) of the reduction smem.
+template <int NV>
+__device__ __forceinline__ void stage_scalars(Ctx& c, const double (&v)[NV]) {
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+    const double x = warp_sum(v[k]);
+    if (c.lane == 0) c.rs.part[c.warp * kRedK + k] = x;
+  }
+}
+
+// Statistics of a factor needed before gathering it: theta needs ||U||_F^2
+// (trace constraint) and the column sums (C = -ee').  On return (all CTAs):
+// *nrm2 and dst_cs[0..s) (dst_cs may be c.cs or another smem array).
+template <int S>
+__device__ __forceinline__ void factor_stats_to(Ctx& c, const Params& P, const double* __restrict__ U,
+                                             int s_rt, double* nrm2, double* dst_cs) {
+  const int s = S > 0 ? S : s_rt;
+  double sq = 0.0;
+  rows_colsum<S>(c, s_rt, 1, [&](int64_t o, int) {
+    const double u = U[o];
+    sq = sq + u * u;
+    return u;
+  });
+  double v[1] = {sq};
+  stage_scalars<1>(c, v);
+  team_reduce_smem(c.t, c.rs, 1 + s);
+  *nrm2 = c.rs.out[0];
+  if (threadIdx.x < (unsigned)s) dst_cs[threadIdx.x] = c.rs.out[1 + threadIdx.x];
   __syncthreads();
+}
+template <int S>
+__device__ __forceinline__ void factor_stats(Ctx& c, const Params& P, const double* __restrict__ U,
+                                             int s_rt, double* nrm2) {
+  factor_stats_to<S>(c, P, U, s_rt, nrm2, c.cs);
 }
 
 // <CU, U> from the statistics: theta -sum_c cs_c^2, MC 0.5||U||^2.
-__device__ __forceinline__ double cdot_from_stats(const Ctx& c, const DevPairs& I, int s,
+__device__ __forceinline__ double cdot_from_stats(const double* cs, const DevPairs& I, int s,
                                                   double nrm2) {
   if (is_theta(I)) {
     double t = 0.0;
-    for (int k = 0; k < s; ++k) t = t + c.cs[k] * c.cs[k];
+    for (int k = 0; k < s; ++k) t = t + cs[k] * cs[k];
     return -t;
   }
   return 0.5 * nrm2;
+}
+__device__ __forceinline__ double cdot_from_stats(const Ctx& c, const DevPairs& I, int s,
+                                                  double nrm2) {
+  return cdot_from_stats(c.cs, I, s, nrm2);
 }
 
 __device__ __forceinline__ double theta_alpha_or_half(const DevPairs& I, double qt) {
@@ -317,7 +429,7 @@ __device__ __forceinline__ double theta_alpha_or_half(const DevPairs& I, double 
 }
 
 template <int S>
-__device__ __noinline__ void copy_rows(Ctx& c, const double* __restrict__ src, double* dst, int s_rt) {
+__device__ __forceinline__ void copy_rows(Ctx& c, const double* __restrict__ src, double* dst, int s_rt) {
   const int s = S > 0 ? S : s_rt;
   for (int64_t a = c.rl + threadIdx.x; a < c.rh; a += kThreads)
     for (int k = 0; k < s; ++k) dst[a * s + k] = src[a * s + k];
@@ -362,20 +474,34 @@ struct FistaOut {
   int iters;
 };
 
+// a of the curvature line search (adap_fista.cpp:49-50)
+__device__ __forceinline__ double fista_a(double tau, double A, double L, double mu) {
+  return (tau + sqrt(tau * tau + 4.0 * tau * A * (L - mu))) / (2.0 * (L - mu));
+}
+
 // fista_run on psi(u) = lambda L_beta(uu';p) + 0.5||u - W||^2 from x0 = W
 // (adap_fista.cpp:14-103, adap_aipp.cpp:20-36).  On success buffers[yn]
 // holds y and buffers[v] holds v.
+//
+// Team passes per iteration (no L-doubling): T2 value+gradient at x~ (row
+// pass), T34 y+ and its map (y+ produced on the fly inside the map so no
+// separate barrier), T5 gradient at y+ fused with the x update and the NEXT
+// iteration's x~ and its statistics.  Three all-reduces per iteration.
 template <int S>
-__device__ __noinline__ bool fista_dev(Ctx& c, const Params& P, Roles& R, int s, double lambda, double L0,
-                          FistaOut& out) {
+__device__ __noinline__ bool fista_dev(Ctx& c, const Params& P, Roles& R, int s, double lambda,
+                                       double L0, FistaOut& out) {
   const DevPairs& I = P.I;
   const Cfg& cf = P.cfg;
-  constexpr int SR = S > 0 ? S : kSMax;
   const double mu = cf.fista_mu, chi = cf.fista_chi, sigma = cf.fista_sigma;
   const double beta = c.beta;
   const double pt = c.p_trace;
+  const bool theta = is_theta(I);
+  // y+ recomputed inside the map (saves a barrier) while the instance is
+  // latency-bound; beyond ~2^20 factor entries the divisions would dominate
+  const bool fuse_y = I.n * (int64_t)s <= (int64_t(1) << 20);
   double A = 0.0, tau = 1.0, L = L0;
-  // x = y = x0
+  double* csx = c.cs + kSMax;  // column sums of x~ (kept apart from c.cs)
+  prof_mark(c, P, kPfAipp);
   {
     const double* W = P.buf[R.wp];
     double* X = P.buf[R.x];
@@ -385,7 +511,10 @@ __device__ __noinline__ bool fista_dev(Ctx& c, const Params& P, Roles& R, int s,
         X[a * s + k] = W[a * s + k];
         Y[a * s + k] = W[a * s + k];
       }
+    __syncthreads();
   }
+  bool pre = false;  // x~ and its statistics already produced by T5
+  double dd = 0.0, nt2 = 0.0;
   for (int it = 0;; ++it) {
     const int cap = cf.fista_max_iters > 0
                         ? cf.fista_max_iters
@@ -394,52 +523,46 @@ __device__ __noinline__ bool fista_dev(Ctx& c, const Params& P, Roles& R, int s,
       out.status = 2;
       out.L = L;
       out.iters = it;
-      // y stays in R.y: callers treat it as failure
       return true;
     }
-    double a, psi_t, psi_n, dsq, dist0, nrmz, ny2;
+    double a, psi_t, psi_n, dsq, dist0, ny2;
     for (;;) {
-      a = (tau + sqrt(tau * tau + 4.0 * tau * A * (L - mu))) / (2.0 * (L - mu));
-      // ---- T1: x_tilde = (A y + a x)/(A + a); ||xt - W||^2; theta stats
+      a = fista_a(tau, A, L, mu);
       const double* W = P.buf[R.wp];
-      const double* X = P.buf[R.x];
-      const double* Y = P.buf[R.y];
       double* XT = P.buf[R.xt];
-      double nt2 = 0.0, dd = 0.0;
-      {
-        double v[SR + 2];
-#pragma unroll
-        for (int k = 0; k < SR + 2; ++k) v[k] = 0.0;
-        for (int64_t r = c.rl + threadIdx.x; r < c.rh; r += kThreads) {
-#pragma unroll
-          for (int k = 0; k < SR; ++k)
-            if (k < s) {
-              const int64_t o = r * s + k;
-              const double xt = (A * Y[o] + a * X[o]) / (A + a);
-              XT[o] = xt;
-              const double dv = xt - W[o];
-              v[0] = v[0] + dv * dv;
-              v[1] = v[1] + xt * xt;
-              v[2 + k] = v[2 + k] + xt;
-            }
-        }
-        team_sum<SR + 2>(c.t, c.rs, v);
-        dd = v[0];
-        nt2 = v[1];
-        if (threadIdx.x < (unsigned)s) c.cs[threadIdx.x] = c.rs.out[2 + threadIdx.x];
+      if (!pre) {
+        // ---- T1: x~ = (A y + a x)/(A + a); ||x~ - W||^2; ||x~||^2, colsum(x~)
+        const double* X = P.buf[R.x];
+        const double* Y = P.buf[R.y];
+        double sc[2] = {0.0, 0.0};
+        rows_colsum<S>(c, s, 2, [&](int64_t o, int) {
+          const double xt = (A * Y[o] + a * X[o]) / (A + a);
+          XT[o] = xt;
+          const double dv = xt - W[o];
+          sc[0] = sc[0] + dv * dv;
+          sc[1] = sc[1] + xt * xt;
+          return xt;
+        });
+        stage_scalars<2>(c, sc);
+        team_reduce_smem(c.t, c.rs, 2 + s);
+        dd = c.rs.out[0];
+        nt2 = c.rs.out[1];
+        if (threadIdx.x < (unsigned)s) csx[threadIdx.x] = c.rs.out[2 + threadIdx.x];
         __syncthreads();
+        prof_mark(c, P, kPfT1);
       }
-      // ---- T2: value_and_gradient at x_tilde fused with psi gradient and
-      //          the projection norm (sdp_instance.cpp:115-127)
+      pre = false;
+      // ---- T2: value_and_gradient at x~ (sdp_instance.cpp:115-127) fused with
+      //          the psi gradient and the projection norm
       double rt = 0.0, qt = 0.0;
-      if (is_theta(I)) {
+      if (theta) {
         rt = nt2 - I.b_trace;
         qt = pt + beta * rt;
       }
       double* GT = P.buf[R.gt];
-      double hU = 0.0, zz = 0.0;
-      double sums[3] = {0.0, 0.0, 0.0};
+      double nrmz;
       {
+        double hU = 0.0, zz = 0.0;
         auto epi = [&](int64_t row, double h, double xo) {
           if (c.lane < s) {
             const int64_t o = row * s + c.lane;
@@ -451,75 +574,77 @@ __device__ __noinline__ bool fista_dev(Ctx& c, const Params& P, Roles& R, int s,
             zz = zz + z * z;
           }
         };
+        double sums[3] = {0.0, 0.0, 0.0};
         row_pass<S, false>(c, P, XT, s, P.p_up, P.p_lo, beta, theta_alpha_or_half(I, qt),
-                           is_theta(I) ? c.cs : nullptr, false, sums, epi);
+                           theta ? csx : nullptr, false, sums, epi);
         double v[5] = {hU, sums[0], sums[1], sums[2], zz};
         team_sum<5>(c.t, c.rs, v);
-        hU = v[0];
+        prof_mark(c, P, kPfT2);
         double pr = v[1], rr = v[2], qrb = v[3];
         zz = v[4];
-        if (is_theta(I)) {
+        if (theta) {
           pr = pr + pt * rt;
           rr = rr + rt * rt;
           qrb = qrb + qt * (rt + I.b_trace);
         }
-        const double cdot = hU - qrb;
+        const double cdot = v[0] - qrb;
         const double val = cdot + pr + 0.5 * beta * rr;
         if (!isfinite(val)) {
           fail(c, kErrNumerical, kMsgAlValGrad);
           return false;
         }
         psi_t = lambda * val + 0.5 * dd;
+        // project_ball (sdp_instance.cpp:94-99)
+        if (!isfinite(zz)) {
+          fail(c, kErrInput, kMsgProjectBall);
+          return false;
+        }
+        nrmz = sqrt(zz);
       }
-      // ---- project_ball (sdp_instance.cpp:94-99)
-      if (!isfinite(zz)) {
-        fail(c, kErrInput, kMsgProjectBall);
-        return false;
-      }
-      nrmz = sqrt(zz);
       const bool scale = !(nrmz <= 1.0);
-      // ---- T3: y_next; ||y-W||^2, ||y-xt||^2, <gt, y-xt>, stats of y
-      double* YN = P.buf[R.yn];
-      double v3[SR + 4];
-#pragma unroll
-      for (int k = 0; k < SR + 4; ++k) v3[k] = 0.0;
-      for (int64_t r = c.rl + threadIdx.x; r < c.rh; r += kThreads) {
-#pragma unroll
-        for (int k = 0; k < SR; ++k)
-          if (k < s) {
-            const int64_t o = r * s + k;
-            const double xt = XT[o], gt = GT[o];
-            const double z = xt - gt / L;
-            const double y = scale ? z / nrmz : z;
-            YN[o] = y;
-            const double d0 = y - W[o];
-            const double dx = y - xt;
-            v3[0] = v3[0] + d0 * d0;
-            v3[1] = v3[1] + dx * dx;
-            v3[2] = v3[2] + gt * dx;
-            v3[3] = v3[3] + y * y;
-            v3[4 + k] = v3[4 + k] + y;
-          }
-      }
-      c.t.sync();
-      // ---- T4: map at y_next (al_value, sdp_instance.cpp:50-60)
-      double ms[2] = {0.0, 0.0};
-      map_pass<S>(c, P, YN, s, kMapPR, P.p_up, nullptr, nullptr, ms);
+      // ---- T34: y+ (written for the row part, produced on the fly for the
+      //           map); ||y-W||^2, ||y-x~||^2, <g~, y-x~>, ||y||^2, colsum(y)
       {
-        double v[SR + 6];
-#pragma unroll
-        for (int k = 0; k < SR + 4; ++k) v[k] = v3[k];
-        v[SR + 4] = ms[0];
-        v[SR + 5] = ms[1];
-        team_sum<SR + 6>(c.t, c.rs, v);
-        dist0 = v[0];
-        dsq = v[1];
-        const double lin_s = v[2];
-        ny2 = v[3];
-        if (threadIdx.x < (unsigned)s) c.cs[threadIdx.x] = c.rs.out[4 + threadIdx.x];
+        double* YN = P.buf[R.yn];
+        double v3[4] = {0.0, 0.0, 0.0, 0.0};
+        rows_colsum<S>(c, s, 6, [&](int64_t o, int) {
+          const double xt = XT[o], gt = GT[o];
+          const double z = xt - gt / L;
+          const double y = scale ? z / nrmz : z;
+          YN[o] = y;
+          const double d0 = y - W[o];
+          const double dx = y - xt;
+          v3[0] = v3[0] + d0 * d0;
+          v3[1] = v3[1] + dx * dx;
+          v3[2] = v3[2] + gt * dx;
+          v3[3] = v3[3] + y * y;
+          return y;
+        });
+        RowSrc src;
+        if (fuse_y) {
+          src.XT = XT;
+          src.GT = GT;
+          src.L = L;
+          src.nrm = nrmz;
+          src.scale = scale;
+        } else {
+          c.t.sync();  // y+ complete before it is gathered
+          src.U = YN;
+        }
+        double ms[2] = {0.0, 0.0};
+        map_pass_src<S>(c, P, src, s, kMapPR, P.p_up, nullptr, nullptr, ms);
+        double v[6] = {v3[0], v3[1], v3[2], v3[3], ms[0], ms[1]};
+        stage_scalars<6>(c, v);
+        team_reduce_smem(c.t, c.rs, 6 + s);
+        prof_mark(c, P, kPfT34);
+        dist0 = c.rs.out[0];
+        dsq = c.rs.out[1];
+        const double lin_s = c.rs.out[2];
+        ny2 = c.rs.out[3];
+        double pr = c.rs.out[4], rr = c.rs.out[5];
+        if (threadIdx.x < (unsigned)s) c.cs[threadIdx.x] = c.rs.out[6 + threadIdx.x];
         __syncthreads();
-        double pr = v[SR + 4], rr = v[SR + 5];
-        if (is_theta(I)) {
+        if (theta) {
           const double r2 = ny2 - I.b_trace;
           pr = pr + pt * r2;
           rr = rr + r2 * r2;
@@ -551,18 +676,20 @@ __device__ __noinline__ bool fista_dev(Ctx& c, const Params& P, Roles& R, int s,
       out.dist0 = dist0;
       return true;
     }
-    // ---- T5: gradient at y_next -> v; x update (adap_fista.cpp:68-71, 86-87)
+    // ---- T5: gradient at y+ -> v; x update (adap_fista.cpp:68-71, 86-87);
+    //          next x~ with the same L and its statistics
     {
       const double* W = P.buf[R.wp];
-      const double* XT = P.buf[R.xt];
+      double* XT = P.buf[R.xt];
       const double* GT = P.buf[R.gt];
       const double* YN = P.buf[R.yn];
       double* X = P.buf[R.x];
       double* V = P.buf[R.v];
       double qt = 0.0;
-      if (is_theta(I)) qt = pt + beta * (ny2 - I.b_trace);
-      double vv = 0.0;
+      if (theta) qt = pt + beta * (ny2 - I.b_trace);
       const double Lm = L - mu, mua = mu * a, tam = tau - a * mu;
+      const double an = fista_a(tau, A_next, L, mu);
+      double vv = 0.0, ddn = 0.0, ntn = 0.0, csn = 0.0;
       auto epi = [&](int64_t row, double h, double yo) {
         if (c.lane < s) {
           const int64_t o = row * s + c.lane;
@@ -573,15 +700,29 @@ __device__ __noinline__ bool fista_dev(Ctx& c, const Params& P, Roles& R, int s,
           V[o] = vt;
           vv = vv + vt * vt;
           const double sd = Lm * (xt - yo);
-          X[o] = (mua * yo + tam * X[o] - a * sd) / tau;
+          const double xn = (mua * yo + tam * X[o] - a * sd) / tau;
+          X[o] = xn;
+          const double xtn = (A_next * yo + an * xn) / (A_next + an);
+          XT[o] = xtn;
+          const double dv = xtn - W[o];
+          ddn = ddn + dv * dv;
+          ntn = ntn + xtn * xtn;
+          csn = csn + xtn;
         }
       };
       double sums[3] = {0.0, 0.0, 0.0};
       row_pass<S, false>(c, P, YN, s, P.p_up, P.p_lo, beta, theta_alpha_or_half(I, qt),
-                         is_theta(I) ? c.cs : nullptr, false, sums, epi);
-      double v[1] = {vv};
-      team_sum<1>(c.t, c.rs, v);
-      vv = v[0];
+                         theta ? c.cs : nullptr, false, sums, epi);
+      double v[3] = {vv, ddn, ntn};
+      stage_scalars<3>(c, v);
+      if (c.lane < s) c.rs.part[c.warp * kRedK + 3 + c.lane] = csn;
+      team_reduce_smem(c.t, c.rs, 3 + s);
+      prof_mark(c, P, kPfT5);
+      vv = c.rs.out[0];
+      dd = c.rs.out[1];
+      nt2 = c.rs.out[2];
+      if (threadIdx.x < (unsigned)s) csx[threadIdx.x] = c.rs.out[3 + threadIdx.x];
+      __syncthreads();
       if (!isfinite(vv)) {
         fail(c, kErrNumerical, kMsgAlGrad);
         return false;
@@ -599,6 +740,7 @@ __device__ __noinline__ bool fista_dev(Ctx& c, const Params& P, Roles& R, int s,
     const int tmp = R.y;
     R.y = R.yn;
     R.yn = tmp;
+    pre = true;
   }
 }
 
@@ -657,6 +799,7 @@ __device__ __noinline__ bool aipp_dev(Ctx& c, const Params& P, Roles& R, int s, 
             v[1] = v[1] + r * r;
           }
         team_sum<2>(c.t, c.rs, v);
+        prof_mark(c, P, kPfAipp);
         if (descent >= v[0]) {
           L_out = fo.L;
           Rn2 = v[1];

@@ -94,6 +94,7 @@ __device__ __noinline__ void solve_dev(Ctx& c, const Params& P, SolveOut* so) {
   const Cfg& cf = P.cfg;
   const double t0 = team_now(c);
   const double deadline = t0 + cf.time_limit * 1e9;
+  if (c.t.rank == 0 && threadIdx.x == 0) c.prof_last = gtimer_ns();
   const double nb1 = I.norm_b1, nb2 = I.nb2;
   const double eps_floor = cf.eps_floor > 0 ? cf.eps_floor : cf.eps * (1.0 + nb1) / 10.0;
   double eps_t = cf.eps0 > 0 ? cf.eps0 : 1e-2 * (1.0 + nb1);
@@ -178,6 +179,7 @@ __device__ __noinline__ void solve_dev(Ctx& c, const Params& P, SolveOut* so) {
     }
     c.p_trace = c.p_trace + beta * ho.rt;
     theta = ho.theta;
+    prof_mark(c, P, kPfOuter);
     if (is_theta(I) && !isfinite(c.p_trace)) bad = 1.0;
     if (bad != 0.0) {
       c.msg = kMsgNonFinite;

@@ -38,35 +38,42 @@ __device__ void emit_trace(const Params& P, Ctx& c, const TraceEv& ev) {
 
 // ---------------------------------------------------------------- Jacobi ---
 // Same rotations, same order, same arithmetic as oracle/src/base.cpp
-// jacobi_eigh: tournament rounds; all row rotations, then column rotations,
-// then pivots zeroed.  Input H column-major with leading dim ldh; outputs
-// ascending c.ev[0..k) and c.E (column-major, ld k), signs normalised.
+// jacobi_eigh: tournament rounds (circle method); per round every thread
+// owns one (pair, row/column) item, computes its pair's rotation from the
+// round-start snapshot, applies the row rotation, then the column rotation
+// (and eigenvector update), zeroing the pivot — three barriers per round.
+// Input H column-major with leading dim ldh; outputs ascending c.ev[0..k)
+// and c.E (column-major, ld k), signs normalised.
 __device__ __noinline__ void jacobi_dev(Ctx& c, const double* H, int ldh, int k) {
-  double* A = c.JA;
-  double* V = c.JV;
-  const int tid = threadIdx.x;
+  double* const A = c.JA;
+  double* const V = c.JV;
+  double* const red = c.rs.part;  // scratch [kWarps]
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   for (int idx = tid; idx < k * k; idx += kThreads) {
     const int i = idx % k, j = idx / k;
     A[idx] = H[i + j * ldh];
     V[idx] = (i == j) ? 1.0 : 0.0;
   }
   __syncthreads();
-  double* red = c.rs.part;  // scratch [kWarps]
   auto block_max = [&](double v) -> double {
     v = warp_max(v);
-    if (c.lane == 0) red[c.warp] = v;
+    if (lane == 0) red[warp] = v;
     __syncthreads();
     double m = red[0];
+#pragma unroll
     for (int w = 1; w < kWarps; ++w) m = fmax(m, red[w]);
     __syncthreads();
     return m;
   };
   if (k > 1) {
     const int kp = k + (k & 1);
+    const int half = kp / 2;
+    // item = (pair t, index r): one per thread (kp/2 <= 16, k <= 32)
+    const int t = tid / k, r = tid % k;
+    const bool active = t < half;
     double mloc = 0.0;
     for (int idx = tid; idx < k * k; idx += kThreads) mloc = fmax(mloc, fabs(A[idx]));
-    const double scale = block_max(mloc);
-    const double thresh = scale * 1e-18;
+    const double thresh = block_max(mloc) * 1e-18;
     for (int sweep = 0; sweep < 40; ++sweep) {
       double oloc = 0.0;
       for (int idx = tid; idx < k * k; idx += kThreads) {
@@ -76,68 +83,45 @@ __device__ __noinline__ void jacobi_dev(Ctx& c, const double* H, int ldh, int k)
       const double off = block_max(oloc);
       if (off <= thresh || off == 0.0) break;
       for (int round = 0; round < kp - 1; ++round) {
-        if (tid == 0) {
-          int np = 0;
-          for (int t = 0; t < kp / 2; ++t) {
-            const int pa = t == 0 ? 0 : 1 + (t - 1 + round) % (kp - 1);
-            const int tb = kp - 1 - t;
-            const int pb = tb == 0 ? 0 : 1 + (tb - 1 + round) % (kp - 1);
-            int x = pa, y = pb;
-            if (x >= k || y >= k) continue;
-            if (x > y) { const int z = x; x = y; y = z; }
-            c.jpq[2 * np] = x;
-            c.jpq[2 * np + 1] = y;
-            ++np;
+        int p = 0, q = 0;
+        bool ok = false;
+        double cc = 1.0, ss = 0.0;
+        if (active) {
+          const int pa = t == 0 ? 0 : 1 + (t - 1 + round) % (kp - 1);
+          const int tb = kp - 1 - t;
+          const int pb = 1 + (tb - 1 + round) % (kp - 1);
+          p = min(pa, pb);
+          q = max(pa, pb);
+          ok = q < k;
+          if (ok) {
+            const double apq = A[p + q * k];
+            if (apq != 0.0) {
+              const double th = (A[q + q * k] - A[p + p * k]) / (2.0 * apq);
+              double tn;
+              if (fabs(th) > 1e150)
+                tn = 0.5 / th;
+              else
+                tn = (th >= 0.0 ? 1.0 : -1.0) / (fabs(th) + sqrt(th * th + 1.0));
+              cc = 1.0 / sqrt(tn * tn + 1.0);
+              ss = tn * cc;
+            }
           }
-          c.jpq[2 * 16] = np;
+        }
+        const bool rot = ok && ss != 0.0;
+        __syncthreads();
+        if (rot) {  // rows p, q at column r
+          const double ap = A[p + r * k], aq = A[q + r * k];
+          A[p + r * k] = cc * ap - ss * aq;
+          A[q + r * k] = ss * ap + cc * aq;
         }
         __syncthreads();
-        const int np = c.jpq[32];
-        if (tid < np) {
-          const int p = c.jpq[2 * tid], q = c.jpq[2 * tid + 1];
-          const double apq = A[p + q * k];
-          double cc = 1.0, ss = 0.0;
-          if (apq != 0.0) {
-            const double th = (A[q + q * k] - A[p + p * k]) / (2.0 * apq);
-            double tn;
-            if (fabs(th) > 1e150)
-              tn = 0.5 / th;
-            else
-              tn = (th >= 0.0 ? 1.0 : -1.0) / (fabs(th) + sqrt(th * th + 1.0));
-            cc = 1.0 / sqrt(tn * tn + 1.0);
-            ss = tn * cc;
-          }
-          c.jcs[2 * tid] = cc;
-          c.jcs[2 * tid + 1] = ss;
-        }
-        __syncthreads();
-        for (int idx = tid; idx < np * k; idx += kThreads) {  // rows
-          const int t = idx / k, j = idx % k;
-          const double cc = c.jcs[2 * t], ss = c.jcs[2 * t + 1];
-          if (ss == 0.0) continue;
-          const int p = c.jpq[2 * t], q = c.jpq[2 * t + 1];
-          const double ap = A[p + j * k], aq = A[q + j * k];
-          A[p + j * k] = cc * ap - ss * aq;
-          A[q + j * k] = ss * ap + cc * aq;
-        }
-        __syncthreads();
-        for (int idx = tid; idx < np * k; idx += kThreads) {  // columns + vectors
-          const int t = idx / k, i = idx % k;
-          const double cc = c.jcs[2 * t], ss = c.jcs[2 * t + 1];
-          if (ss == 0.0) continue;
-          const int p = c.jpq[2 * t], q = c.jpq[2 * t + 1];
-          const double ap = A[i + p * k], aq = A[i + q * k];
-          A[i + p * k] = cc * ap - ss * aq;
-          A[i + q * k] = ss * ap + cc * aq;
-          const double vp = V[i + p * k], vq = V[i + q * k];
-          V[i + p * k] = cc * vp - ss * vq;
-          V[i + q * k] = ss * vp + cc * vq;
-        }
-        __syncthreads();
-        if (tid < np && c.jcs[2 * tid + 1] != 0.0) {
-          const int p = c.jpq[2 * tid], q = c.jpq[2 * tid + 1];
-          A[p + q * k] = 0.0;
-          A[q + p * k] = 0.0;
+        if (rot) {  // columns p, q at row r, eigenvectors, pivot zeroed
+          const double ap = A[r + p * k], aq = A[r + q * k];
+          A[r + p * k] = (r == q) ? 0.0 : cc * ap - ss * aq;
+          A[r + q * k] = (r == p) ? 0.0 : ss * ap + cc * aq;
+          const double vp = V[r + p * k], vq = V[r + q * k];
+          V[r + p * k] = cc * vp - ss * vq;
+          V[r + q * k] = ss * vp + cc * vq;
         }
         __syncthreads();
       }
@@ -182,69 +166,142 @@ __device__ __forceinline__ double* slot_ptr(const Params& P, int sl) {
   return P.vslot + (size_t)sl * P.I.n;
 }
 
-// dst = -(C v + A*(q) v) for v in slot sv (apply_B, lanczos.cpp:38); the
-// caller has team-synchronised after v was written.
-__device__ __noinline__ void lz_apply(Ctx& c, const Params& P, const GOp& g, int sv, double* dst) {
+// A Lanczos vector that exists only as (src / scale): materialised into its
+// slot by the matvec that consumes it, so normalisation costs no barrier.
+struct Pending {
+  const double* src;
+  double scale;
+  double sum;  // column sum of src / scale (theta C-term)
+  int dst;     // slot receiving src / scale (-1: none)
+};
+
+// out = -(C v + A*(q) v) with v = pend.src / pend.scale gathered on the fly
+// (apply_B, lanczos.cpp:38); also writes v into slot pend.dst for own rows.
+// The caller has team-synchronised after pend.src was written.
+__device__ __forceinline__ void lz_apply(Ctx& c, const Params& P, const GOp& g, const Pending& pv,
+                                      double* out) {
   const DevPairs& I = P.I;
-  const double* v = slot_ptr(P, sv);
-  auto epi = [&](int64_t a, double h, double) {
-    if (c.lane == 0) dst[a] = -h;
-  };
-  double sums[3] = {0.0, 0.0, 0.0};
-  row_pass<1, true>(c, P, v, 1, g.qup, g.qlo, 0.0, theta_alpha_or_half(I, g.qt),
-                    is_theta(I) ? &c.vsum[sv] : nullptr, false, sums, epi);
+  const int64_t n = I.n;
+  (void)n;
+  const double* src = pv.src;
+  const double sc = pv.scale;
+  double* vdst = pv.dst >= 0 ? slot_ptr(P, pv.dst) : nullptr;
+  const double alpha = theta_alpha_or_half(I, g.qt);
+  const bool theta = is_theta(I);
+  const int lane = c.lane;
+  double* tile = c.tile;
+  for (int64_t a = c.rl + c.warp; a < c.rh; a += kWarps) {
+    const double va = src[a] / sc;
+    if (vdst && lane == 0) vdst[a] = va;
+    double acc = alpha * va;
+    if (theta) acc = acc - pv.sum;
+    const int64_t lo0 = I.lo_ptr[a], nlo = I.lo_ptr[a + 1] - lo0;
+    const int64_t up0 = I.up_ptr[a], nup = I.up_ptr[a + 1] - up0;
+    const int64_t tot = nlo + nup;
+    for (int64_t base = 0; base < tot; base += 32) {
+      const int64_t e = base + lane;
+      const bool valid = e < tot;
+      double w = 0.0, vb = 0.0;
+      if (valid) {
+        int64_t b;
+        if (e < nlo) {
+          b = I.lo_col[lo0 + e];
+          w = 0.5 * g.qlo[lo0 + e];
+        } else {
+          const int64_t k = up0 + (e - nlo);
+          b = I.ej[k];
+          w = 0.5 * g.qup[k];
+        }
+        vb = src[b] / sc;
+      }
+      const unsigned skip = __ballot_sync(kFull, !valid || w == 0.0);
+      tile[lane] = w * vb;
+      __syncwarp();
+      if (lane == 0) {
+        const int cnt = (int)min((int64_t)32, tot - base);
+        for (int j = 0; j < cnt; ++j)
+          if (!((skip >> j) & 1u)) acc = acc + tile[j];
+      }
+      __syncwarp();
+    }
+    if (lane == 0) out[a] = -acc;
+  }
   __syncthreads();
 }
 
-// h[i] = V_i . w for i < k  (result in c.rs.out[0..k))
-__device__ __noinline__ void lz_dot(Ctx& c, const Params& P, int k, const double* w) {
+// sum_i V_i(a) e_i in increasing i, with the loads issued in batches of 8
+__device__ __forceinline__ double lz_row_dot(const Ctx& c, const Params& P, int k, int64_t a,
+                                             const double* e) {
+  double s = 0.0;
+  int i = 0;
+  for (; i + 8 <= k; i += 8) {
+    double v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = slot_ptr(P, c.col[i + u])[a];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) s = s + v[u] * e[i + u];
+  }
+  for (; i < k; ++i) s = s + slot_ptr(P, c.col[i])[a] * e[i];
+  return s;
+}
+
+// h[i] = V_i . w for i < k  (result in c.rs.out[0..k)).  Lane i owns basis
+// vector i and walks the warp's 32-row chunk sequentially (rows broadcast by
+// shuffle): no per-vector warp reductions, fixed summation order.
+__device__ __forceinline__ void lz_dot(Ctx& c, const Params& P, int k, const double* w) {
+  const int lane = c.lane;
+  const int64_t rl = c.rl, rh = c.rh;
+  const double* vi = slot_ptr(P, c.col[lane < k ? lane : 0]);
   double mine = 0.0;
-  for (int64_t a0 = c.rl + c.warp * 32; a0 < c.rh; a0 += kWarps * 32) {
-    const int64_t a = a0 + c.lane;
-    const bool ok = a < c.rh;
-    const double wa = ok ? w[a] : 0.0;
-    for (int i = 0; i < k; ++i) {
-      double t = ok ? slot_ptr(P, c.col[i])[a] * wa : 0.0;
-      t = warp_sum(t);
-      if (c.lane == i) mine = mine + t;
+  for (int64_t a0 = rl + c.warp * 32; a0 < rh; a0 += kWarps * 32) {
+    const int cnt = (int)min((int64_t)32, rh - a0);
+    const double wl = lane < cnt ? w[a0 + lane] : 0.0;
+#pragma unroll 8
+    for (int r = 0; r < 32; ++r) {
+      const double wr = __shfl_sync(kFull, wl, r);
+      if (r < cnt && lane < k) mine = mine + vi[a0 + r] * wr;
     }
   }
   team_sum_lanes(c.t, c.rs, mine, k);
 }
-// w -= V_k h; then (dot_after) h2 = V_k' w  or  ||w||^2.  h read from smem.
-__device__ __noinline__ void lz_sub(Ctx& c, const Params& P, int k, double* w, const double* h,
-                       bool dot_after) {
-  double mine = 0.0;
-  for (int64_t a0 = c.rl + c.warp * 32; a0 < c.rh; a0 += kWarps * 32) {
-    const int64_t a = a0 + c.lane;
-    const bool ok = a < c.rh;
+// w -= V_k h (thread per row, ordered over the basis); then h2 = V_k' w
+// (dot_after) or (||w||^2, sum w) into rs.out[0..2)
+__device__ __forceinline__ void lz_sub(Ctx& c, const Params& P, int k, double* w, const double* h,
+                                       bool dot_after) {
+  const int lane = c.lane;
+  const int64_t rl = c.rl, rh = c.rh;
+  const double* vi = slot_ptr(P, c.col[lane < k ? lane : 0]);
+  double mine = 0.0, ssum = 0.0;
+  for (int64_t a0 = rl + c.warp * 32; a0 < rh; a0 += kWarps * 32) {
+    const int64_t a = a0 + lane;
+    const int cnt = (int)min((int64_t)32, rh - a0);
     double wn = 0.0;
-    if (ok) {
-      double s = 0.0;
-      for (int i = 0; i < k; ++i) s = s + slot_ptr(P, c.col[i])[a] * h[i];
-      wn = w[a] - s;
+    if (a < rh) {
+      wn = w[a] - lz_row_dot(c, P, k, a, h);
       w[a] = wn;
     }
     if (dot_after) {
-      for (int i = 0; i < k; ++i) {
-        double t = ok ? slot_ptr(P, c.col[i])[a] * wn : 0.0;
-        t = warp_sum(t);
-        if (c.lane == i) mine = mine + t;
+#pragma unroll 8
+      for (int r = 0; r < 32; ++r) {
+        const double wr = __shfl_sync(kFull, wn, r);
+        if (r < cnt && lane < k) mine = mine + vi[a0 + r] * wr;
       }
     } else {
       mine = mine + wn * wn;
+      ssum = ssum + wn;
     }
   }
   if (dot_after) {
     team_sum_lanes(c.t, c.rs, mine, k);
   } else {
-    double v[1] = {mine};
-    team_sum<1>(c.t, c.rs, v);
+    double v[2] = {mine, ssum};
+    team_sum<2>(c.t, c.rs, v);
   }
 }
 // orthogonalize (lanczos.cpp:22-28): h <- V'w; w -= Vh; h2 <- V'w; w -= Vh2;
-// h += h2.  Returns ||w||^2; h left in hh[0..k).
-__device__ __noinline__ double lz_cgs2(Ctx& c, const Params& P, int k, double* w, double* hh, double* hh2) {
+// h += h2.  Returns ||w||^2 (and *wsum = sum w); h left in hh[0..k).
+__device__ __noinline__ double lz_cgs2(Ctx& c, const Params& P, int k, double* w, double* hh,
+                                       double* hh2, double* wsum) {
   lz_dot(c, P, k, w);
   if (threadIdx.x < (unsigned)k) hh[threadIdx.x] = c.rs.out[threadIdx.x];
   __syncthreads();
@@ -253,42 +310,32 @@ __device__ __noinline__ double lz_cgs2(Ctx& c, const Params& P, int k, double* w
   __syncthreads();
   lz_sub(c, P, k, w, hh2, false);
   const double ww = c.rs.out[0];
+  *wsum = c.rs.out[1];
   __syncthreads();
   if (threadIdx.x < (unsigned)k) hh[threadIdx.x] = hh[threadIdx.x] + hh2[threadIdx.x];
   __syncthreads();
   return ww;
 }
-// slot dst = src / nrm ; vsum[dst] = sum (team-reduced)
-__device__ __noinline__ void lz_scale_into(Ctx& c, const Params& P, const double* src, double nrm, int dst) {
+// slot dst = V_f e (e in smem, column of c.E); returns ||.||^2 and the sum
+__device__ __forceinline__ double lz_combine(Ctx& c, const Params& P, int f, const double* e, int dst,
+                                          double* sum) {
   double* d = slot_ptr(P, dst);
-  double v[1] = {0.0};
+  double v[2] = {0.0, 0.0};
   for (int64_t a = c.rl + threadIdx.x; a < c.rh; a += kThreads) {
-    const double x = src[a] / nrm;
-    d[a] = x;
-    v[0] = v[0] + x;
-  }
-  team_sum<1>(c.t, c.rs, v);
-  if (threadIdx.x == 0) c.vsum[dst] = v[0];
-  __syncthreads();
-}
-// slot dst = V_f e (e in smem, column of c.E); returns ||.||^2
-__device__ __noinline__ double lz_combine(Ctx& c, const Params& P, int f, const double* e, int dst) {
-  double* d = slot_ptr(P, dst);
-  double v[1] = {0.0};
-  for (int64_t a = c.rl + threadIdx.x; a < c.rh; a += kThreads) {
-    double s = 0.0;
-    for (int i = 0; i < f; ++i) s = s + slot_ptr(P, c.col[i])[a] * e[i];
+    const double s = lz_row_dot(c, P, f, a, e);
     d[a] = s;
     v[0] = v[0] + s * s;
+    v[1] = v[1] + s;
   }
-  team_sum<1>(c.t, c.rs, v);
+  team_sum<2>(c.t, c.rs, v);
+  *sum = v[1];
   return v[0];
 }
 
 // min_eigenpair (lanczos.cpp:32-141) of op = C + A*(q), i.e. B = -op.
-// Slots used: c.col[] basis, plus scratch; returns the best pair's slot.
-__device__ __noinline__ bool lanczos_dev(Ctx& c, const Params& P, const GOp& g, double tol, int max_iters,
-                            int block_restart, LzOut& best) {
+// Per matvec: one gather pass (no barrier) + three all-reduces (CGS2).
+__device__ __noinline__ bool lanczos_dev(Ctx& c, const Params& P, const GOp& g, double tol,
+                                         int max_iters, int block_restart, LzOut& best) {
   const DevPairs& I = P.I;
   const int64_t n = I.n;
   const int kmax = (int)min((int64_t)block_restart, n);
@@ -308,18 +355,22 @@ __device__ __noinline__ bool lanczos_dev(Ctx& c, const Params& P, const GOp& g, 
     if (sl >= 0) used &= ~(1ull << sl);
   };
   int refill = 0;
-  // V(:,0) = v0/|v0|
+  const int wslot[2] = {alloc(), alloc()};  // ping-pong w buffers
+  int wc = 0;
+  Pending pend;
   {
-    double v[1] = {0.0};
+    // V(:,0) = v0/|v0|
+    double v[2] = {0.0, 0.0};
     for (int64_t a = c.rl + threadIdx.x; a < c.rh; a += kThreads) {
       const double x = P.lz_rand[a];
       v[0] = v[0] + x * x;
+      v[1] = v[1] + x;
     }
-    team_sum<1>(c.t, c.rs, v);
+    team_sum<2>(c.t, c.rs, v);
     const int s0 = alloc();
     if (threadIdx.x == 0) c.col[0] = s0;
-    __syncthreads();
-    lz_scale_into(c, P, P.lz_rand, sqrt(v[0]), s0);
+    const double nv = sqrt(v[0]);
+    pend = Pending{P.lz_rand, nv, v[1] / nv, s0};
   }
   for (int idx = threadIdx.x; idx < kHLd * kHLd; idx += kThreads) c.H[idx] = 0.0;
   __syncthreads();
@@ -327,16 +378,20 @@ __device__ __noinline__ bool lanczos_dev(Ctx& c, const Params& P, const GOp& g, 
   double beta = 0.0;
   best = LzOut();
   best.residual = INFINITY;
-  const int wslot = alloc();  // holds w across restarts
-  double* w = slot_ptr(P, wslot);
+  double* w = slot_ptr(P, wslot[wc]);
 
   for (;;) {
     bool breakdown = false;
     while (filled < basis && matvecs < max_iters) {
       const int j = filled;
-      lz_apply(c, P, g, c.col[j], w);
+      w = slot_ptr(P, wslot[wc]);
+      lz_apply(c, P, g, pend, w);  // materialises V(:, j) = pending column
+      prof_mark(c, P, kPfLzApply);
+      if (threadIdx.x == 0) c.vsum[pend.dst] = pend.sum;
       ++matvecs;
-      const double ww = lz_cgs2(c, P, basis, w, hh, hh2);
+      double wsum;
+      const double ww = lz_cgs2(c, P, basis, w, hh, hh2, &wsum);
+      prof_mark(c, P, kPfLzCgs);
       if (threadIdx.x < (unsigned)basis) {
         c.H[threadIdx.x + j * kHLd] = hh[threadIdx.x];
         c.H[j + threadIdx.x * kHLd] = hh[threadIdx.x];
@@ -358,37 +413,30 @@ __device__ __noinline__ bool lanczos_dev(Ctx& c, const Params& P, const GOp& g, 
           c.H[j + basis * kHLd] = beta;
         }
         __syncthreads();
-        lz_scale_into(c, P, w, beta, sl);
+        pend = Pending{w, beta, wsum / beta, sl};
+        wc ^= 1;
         ++basis;
       }
     }
     const int f = filled;
     jacobi_dev(c, c.H, kHLd, f);
+    prof_mark(c, P, kPfJacobi);
     const int top = f - 1;
     const double mu = c.ev[top];
     const double res_est = breakdown ? 0.0 : beta * fabs(c.E[(f - 1) + top * f]);
     const bool budget_left = matvecs + 1 < max_iters;
     if (res_est <= tol * fmax(1.0, fabs(mu)) || !budget_left || (breakdown && filled >= n)) {
-      // measure(V_f * e_top)
-      const int xs = alloc();
-      const double nx2 = lz_combine(c, P, f, c.E + top * f, xs);
-      {
-        double* x = slot_ptr(P, xs);
-        const double nx = sqrt(nx2);
-        double v[1] = {0.0};
-        for (int64_t a = c.rl + threadIdx.x; a < c.rh; a += kThreads) {
-          const double t = x[a] / nx;
-          x[a] = t;
-          v[0] = v[0] + t;
-        }
-        team_sum<1>(c.t, c.rs, v);
-        if (threadIdx.x == 0) c.vsum[xs] = v[0];
-        __syncthreads();
-      }
+      // measure(V_f * e_top) (lanczos.cpp:61-74)
+      const int xr = alloc();  // raw Ritz vector
+      double xsum;
+      const double nx2 = lz_combine(c, P, f, c.E + top * f, xr, &xsum);
+      const double nx = sqrt(nx2);
+      const int xs = alloc();  // normalised copy, materialised by the matvec
       const int bs = alloc();
       double* Bx = slot_ptr(P, bs);
-      lz_apply(c, P, g, xs, Bx);
+      lz_apply(c, P, g, Pending{slot_ptr(P, xr), nx, xsum / nx, xs}, Bx);
       ++matvecs;
+      release(xr);
       const double* x = slot_ptr(P, xs);
       double v1[1] = {0.0};
       for (int64_t a = c.rl + threadIdx.x; a < c.rh; a += kThreads) v1[0] = v1[0] + x[a] * Bx[a];
@@ -414,12 +462,13 @@ __device__ __noinline__ bool lanczos_dev(Ctx& c, const Params& P, const GOp& g, 
         release(xs);
       }
       best.matvecs = matvecs;
+      prof_mark(c, P, kPfLzMeasure);
       if (best.converged || matvecs >= max_iters || (breakdown && filled >= n)) {
         best.matvecs = matvecs;
         return true;
       }
     }
-    // thick restart
+    // thick restart (lanczos.cpp:117-139)
     const int l = min(keep, f - 1 > 0 ? f - 1 : 1);
     int newcol[kLanczosMax];
     {
@@ -428,7 +477,6 @@ __device__ __noinline__ bool lanczos_dev(Ctx& c, const Params& P, const GOp& g, 
         fail(c, kErrCapacity, kMsgRefillCap);
         return false;
       }
-      // kept_t = V_f E[:, f-1-t], column sums per t
       double mine = 0.0;
       for (int64_t a0 = c.rl + c.warp * 32; a0 < c.rh; a0 += kWarps * 32) {
         const int64_t a = a0 + c.lane;
@@ -436,8 +484,7 @@ __device__ __noinline__ bool lanczos_dev(Ctx& c, const Params& P, const GOp& g, 
         for (int t = 0; t < l; ++t) {
           double s = 0.0;
           if (ok) {
-            const double* e = c.E + (f - 1 - t) * f;
-            for (int i = 0; i < f; ++i) s = s + slot_ptr(P, c.col[i])[a] * e[i];
+            s = lz_row_dot(c, P, f, a, c.E + (f - 1 - t) * f);
             slot_ptr(P, newcol[t])[a] = s;
           }
           const double ts = warp_sum(s);
@@ -457,31 +504,41 @@ __device__ __noinline__ bool lanczos_dev(Ctx& c, const Params& P, const GOp& g, 
     }
     __syncthreads();
     const int sl = alloc();
+    if (threadIdx.x == 0) c.col[l] = sl;
+    __syncthreads();
+    const int w_idx = (w == slot_ptr(P, wslot[0])) ? 0 : 1;  // buffer holding the last w
     if (breakdown) {
       if (refill >= P.n_refill) {
         fail(c, kErrCapacity, kMsgRefillCap);
         return false;
       }
       ++refill;
-      const double* fr = P.lz_rand + (size_t)refill * n;
-      for (int64_t a = c.rl + threadIdx.x; a < c.rh; a += kThreads) w[a] = fr[a];
+      // fresh direction: next gaussian_vector of the same stream, orthogonalised
+      double* fr = slot_ptr(P, wslot[1 - w_idx]);
+      const double* rnd = P.lz_rand + (size_t)refill * n;
+      for (int64_t a = c.rl + threadIdx.x; a < c.rh; a += kThreads) fr[a] = rnd[a];
       __syncthreads();
-      const double fn2 = lz_cgs2(c, P, l, w, hh, hh2);
+      double fsum;
+      const double fn2 = lz_cgs2(c, P, l, fr, hh, hh2, &fsum);
       const double fn = sqrt(fn2);
       if (fn <= 1e-13) {
         best.matvecs = matvecs;
         return true;
       }
-      if (threadIdx.x == 0) c.col[l] = sl;
-      __syncthreads();
-      lz_scale_into(c, P, w, fn, sl);
+      pend = Pending{fr, fn, fsum / fn, sl};
+      wc = w_idx;
     } else {
-      if (threadIdx.x == 0) c.col[l] = sl;
-      __syncthreads();
-      lz_scale_into(c, P, w, beta, sl);
+      pend = Pending{w, beta, 0.0, sl};
+      // sum of w/beta: w is the last CGS output
+      double v[1] = {0.0};
+      for (int64_t a = c.rl + threadIdx.x; a < c.rh; a += kThreads) v[0] = v[0] + w[a];
+      team_sum<1>(c.t, c.rs, v);
+      pend.sum = v[0] / beta;
+      wc = 1 - w_idx;
     }
     basis = l + 1;
     filled = l;
+    prof_mark(c, P, kPfLzRestart);
   }
 }
 
@@ -596,6 +653,7 @@ __device__ __noinline__ bool hlr_dev(Ctx& c, const Params& P, Roles& R, int s, d
     double pr = 0, rr = 0, rt = 0, qt = 0;
     HALLAR_DISPATCH_S(s, ok = gradop_dev<S_>(c, P, Y, s, beta, &pr, &rr, &rt, &qt));
     if (!ok) return false;
+    prof_mark(c, P, kPfGradop);
     const GOp g{P.q_up, P.q_lo, qt};
     LzOut lz;
     if (!lanczos_dev(c, P, g, 0.1 * eps_t, cf.eig_max_iters, cf.eig_block_restart, lz))
@@ -620,6 +678,7 @@ __device__ __noinline__ bool hlr_dev(Ctx& c, const Params& P, Roles& R, int s, d
     const bool done = gap <= eps_t;
     const bool no_steps = step >= cf.max_fw_steps;
     const bool no_time = team_now(c) >= (double)deadline_ns;
+    prof_mark(c, P, kPfGap);
     if (done || no_steps || no_time || !lz.converged) {
       out.y_buf = ybuf;
       out.s = s;
@@ -677,6 +736,7 @@ __device__ __noinline__ bool hlr_dev(Ctx& c, const Params& P, Roles& R, int s, d
     }
     s = s_new;
     ++out.fw_steps;
+    prof_mark(c, P, kPfFwStep);
     if (cf.trace) {
       double al;
       HALLAR_DISPATCH_S(s, ok = al_value_dev<S_>(c, P, P.buf[R.yt], s, P.p_up, c.p_trace, beta,

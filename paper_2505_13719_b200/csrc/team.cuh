@@ -41,11 +41,12 @@ struct Team {
     if (threadIdx.x == 0) {
       epoch += 1;
       const unsigned long long target = epoch * (unsigned long long)size;
-      __threadfence();
-      atomicAdd(bar, 1ULL);
+      // release-add publishes this CTA's writes (ordered before by bar.sync)
+      asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(bar), "l"(1ULL) : "memory");
+      // acquire poll: each ld.acquire.gpu invalidates this SM's L1 (CCTL.IVALL),
+      // so no trailing fence is needed before the CTA reads other CTAs' data
       while (ld_acquire_u64(bar) < target) {
       }
-      __threadfence();
     }
     __syncthreads();
   }
@@ -71,12 +72,16 @@ __device__ __forceinline__ void team_reduce_smem(Team& t, RedSmem& rs, int K) {
   const double* base = t.slots + (size_t)t.parity * t.size * kRedK;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int k = warp; k < K; k += kWarps) {
-    double acc = 0.0;
-    int r = lane;
-    if (r < t.size) {
-      acc = __ldcg(base + (size_t)r * kRedK + k);
-      for (r += 32; r < t.size; r += 32) acc = acc + __ldcg(base + (size_t)r * kRedK + k);
+    // all partial loads issued before the (fixed-order) sum: one L2 round trip
+    double v[kMaxTeam / 32];
+#pragma unroll
+    for (int q = 0; q < kMaxTeam / 32; ++q) {
+      const int r = lane + 32 * q;
+      v[q] = (r < t.size) ? __ldcg(base + (size_t)r * kRedK + k) : 0.0;
     }
+    double acc = v[0];
+#pragma unroll
+    for (int q = 1; q < kMaxTeam / 32; ++q) acc = acc + v[q];
     acc = warp_sum(acc);
     if (lane == 0) rs.out[k] = acc;
   }

@@ -38,8 +38,16 @@ __global__ void __launch_bounds__(kThreads, 1)
   sm += kWarps * kRedK;
   c.rs.out = sm;
   sm += kRedK;
-  c.tile = sm + c.warp * kTile * kTileLd;
-  sm += kWarps * kTile * kTileLd;
+  c.tw = sm;
+  sm += kGroups * kTileEntries;
+  c.tterm = sm;
+  sm += kGroups * 4 * kTileEntries;
+  c.vlo = reinterpret_cast<int64_t*>(sm);
+  sm += 2 * kGroups * (kTileRows + 1);
+  c.vup = reinterpret_cast<int64_t*>(sm);
+  sm += 2 * kGroups * (kTileRows + 1);
+  c.tcol = reinterpret_cast<int32_t*>(sm);
+  sm += kGroups * kTileEntries / 2;
   c.cs = sm;
   sm += 2 * kSMax;
   c.H = sm;
@@ -64,8 +72,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   c.col = ip;
   ip += 40;
   c.jpq = ip;
-  c.rl = row_split(P.I, c.t.rank, c.t.size);
-  c.rh = row_split(P.I, c.t.rank + 1, c.t.size);
+  c.tl = P.I.ntiles * c.t.rank / c.t.size;
+  c.th = P.I.ntiles * (c.t.rank + 1) / c.t.size;
+  c.rl = P.I.tile_row[c.tl];
+  c.rh = P.I.tile_row[c.th];
   c.kl = P.I.np * c.t.rank / c.t.size;
   c.kh = P.I.np * (c.t.rank + 1) / c.t.size;
   if (P.op == kOpSolve) {
@@ -103,7 +113,9 @@ namespace {
 thread_local std::string g_err;
 
 constexpr size_t kSmemBytes =
-    sizeof(double) * (kWarps * kRedK + kRedK + kWarps * kTile * kTileLd + 2 * kSMax + kHLd * kHLd +
+    sizeof(double) * (kWarps * kRedK + kRedK + kGroups * (5 * kTileEntries + 4 * (kTileRows + 1) +
+                                                        kTileEntries / 2) +
+                      2 * kSMax + kHLd * kHLd +
                       3 * 32 * 32 + 4 * 32 + 64) +
     sizeof(int) * 80;
 
@@ -159,7 +171,7 @@ struct cuhallar_instance {
   std::vector<int64_t> lo_eid_host;
   // device arrays
   int32_t *ei = nullptr, *ej = nullptr, *lo_col = nullptr;
-  int64_t *up_ptr = nullptr, *lo_ptr = nullptr, *lo_eid = nullptr;
+  int64_t *up_ptr = nullptr, *lo_ptr = nullptr, *lo_eid = nullptr, *tile_row = nullptr;
   double *b_up = nullptr, *b_lo = nullptr;      // scaled b/tau (solve)
   double *ub_up = nullptr, *ub_lo = nullptr;    // unscaled b (operator ABI), lazy
   // workspace
@@ -188,7 +200,7 @@ struct cuhallar_instance {
     auto f = [](void* p) {
       if (p) cudaFree(p);
     };
-    f(ei); f(ej); f(lo_col); f(up_ptr); f(lo_ptr); f(lo_eid); f(b_up); f(b_lo); f(ub_up); f(ub_lo);
+    f(ei); f(ej); f(lo_col); f(up_ptr); f(lo_ptr); f(lo_eid); f(tile_row); f(b_up); f(b_lo); f(ub_up); f(ub_lo);
     f(bar); f(slots); for (auto* b : buf) f(b); f(vslot);
     f(p_up); f(p_lo); f(q_up); f(q_lo); f(r_up); f(r_lo); f(lz_rand); f(dscal); f(discal); f(dso); f(dprof);
     if (trace_host) cudaFreeHost(trace_host);
@@ -235,6 +247,35 @@ void upload_pairs(cuhallar_instance* in) {
   in->lo_col = dupload(lo_col, &in->bytes);
   in->lo_eid = dupload(lo_eid, &in->bytes);
   in->lo_eid_host = std::move(lo_eid);
+  {
+    // Row tiles for the tile engine: consecutive rows, <= kTileRows rows and
+    // <= target entries, target chosen so that every CTA gets tiles.
+    int team = 148;
+    try {
+      team = grid_size(0);
+    } catch (...) {
+    }
+    const int64_t total = 2 * np;
+    const int64_t target =
+        std::max<int64_t>(32, std::min<int64_t>(kTileEntries, (total + team * kGroups - 1) / (team * kGroups)));
+    std::vector<int64_t> tr{0};
+    int64_t r0 = 0;
+    while (r0 < n) {
+      int64_t r1 = r0, ent = 0;
+      while (r1 < n && r1 - r0 < kTileRows) {
+        const int64_t d = (up[r1 + 1] - up[r1]) + (lo[r1 + 1] - lo[r1]);
+        if (r1 > r0 && ent + d > target) break;
+        ent += d;
+        ++r1;
+        if (ent > kTileEntries) break;  // a single long row becomes its own tile
+      }
+      tr.push_back(r1);
+      r0 = r1;
+    }
+    in->tile_row = dupload(tr, &in->bytes);
+    in->I.tile_row = in->tile_row;
+    in->I.ntiles = int64_t(tr.size()) - 1;
+  }
   in->h2d += in->bytes;
   DevPairs& I = in->I;
   I.family = h.family;

@@ -13,6 +13,10 @@ constexpr int kRedK = 40;                // max values per team reduction
 constexpr int kNBuf = 12;                // n x kSMax factor buffers in the pool
 constexpr int kTile = 8;                 // columns per fold chunk
 constexpr int kMaxTeam = 320;            // max persistent CTAs (team reduction width)
+constexpr int kGroups = 4;               // independent 128-thread tile groups per CTA
+constexpr int kGT = kThreads / kGroups;  // threads per tile group
+constexpr int kTileEntries = 512;        // entries per row tile (per group)
+constexpr int kTileRows = 32;            // rows per row tile
 
 enum Family : int { kTheta = 0, kMatcomp = 1, kPhaseret = 2 };
 
@@ -51,6 +55,8 @@ struct DevPairs {
   const double* b_up = nullptr;  // scaled b (edge order), null = all zero
   const double* b_lo = nullptr;  // scaled b (lower order)
   double b_trace = 0.0;          // scaled b[m-1] (theta)
+  const int64_t* tile_row = nullptr;  // [ntiles+1] first row of each row tile
+  int64_t ntiles = 0;
   double norm_b1 = 0.0, nb2 = 0.0, norm_C1 = 0.0;  // scaled instance norms
 };
 

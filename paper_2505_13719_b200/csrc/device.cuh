@@ -37,7 +37,11 @@ enum Msg : int {
 struct Ctx {
   Team t;
   RedSmem rs;
-  double* tile;   // this warp's fold tile [kTile][kTileLd]
+  int64_t* vlo;   // tile engine: [kTileRows+1] lower row pointers of the tile
+  int64_t* vup;   // [kTileRows+1] upper row pointers
+  double* tw;     // [kTileEntries] w per entry
+  int32_t* tcol;  // [kTileEntries] gathered row per entry
+  double* tterm;  // [kTileEntries * 4] w * U(b, c), c < 4
   double* cs;     // [kSMax] column sums of the gathered factor (theta C-term)
   double* H;      // [kHLd][kHLd] Lanczos projected matrix (column-major)
   double* JA;     // [32*32] Jacobi work
@@ -48,7 +52,8 @@ struct Ctx {
   int* jpq;       // [32] pair indices
   double* vsum;   // [nslot] column sums of Lanczos slots (theta)
   int* col;       // [kHLd+1] Lanczos basis -> slot
-  int64_t rl, rh;  // rows owned by this CTA (nnz-balanced)
+  int64_t tl, th;  // row tiles owned by this CTA
+  int64_t rl, rh;  // rows owned by this CTA (= its tiles' rows)
   int64_t kl, kh;  // edges owned by this CTA
   double* hh;     // [32] Lanczos CGS coefficients
   double* hh2;    // [32]
@@ -101,101 +106,312 @@ __device__ int64_t row_split(const DevPairs& I, int rank, int size) {
   return lo;
 }
 
-// ------------------------------------------------------------- row pass ---
-// For every row a owned by this CTA compute, lane c < s,
-//   h(a,c) = init(a,c) (+)fold_k 0.5 q_k U(b_k,c)        (k increasing)
-// where q_k = P_k (FIXED) or q_k = P_k + beta (U_a.U_b - b_k) (!FIXED), the
-// reference's C_plus_adjoint / adjoint_into (instances.cpp:39-55, 99-110,
-// 222-232).  init = alpha*U(a,c) - cs[c] (cs may be null) or 0.
-// !FIXED also accumulates over upper entries (each constraint once):
+// ---------------------------------------------------------- tile engine ---
+// The CTA walks its tiles (host-precomputed runs of consecutive rows with
+// <= kTileEntries entries and <= kTileRows rows).  Per tile:
+//   1. row pointers of the tile -> smem;
+//   2. every thread takes entries v = tid, tid+512, ... of the tile's merged
+//      (lower-then-upper per row) entry list: loads col / multiplier / b,
+//      gathers U_b (and U_a), computes w_v = 0.5 q_v and the products
+//      w_v U(b_v, c) for c < 4 into smem — all entries in flight at once;
+//   3. one thread per (row, column) folds the products of its row in entry
+//      (= increasing constraint k) order and runs the epilogue.
+// The fold adds the same rounded products in the same order as the reference
+// adjoint_into (instances.cpp:45-52), so the pair adjoint stays bit-exact.
+// Column index of a thread in phase 3 is fixed (tid % s), so per-column
+// epilogue accumulators are plain registers.
+//
+// For every row a owned by this CTA and column c:
+//   h(a,c) = init(a,c) (+)fold_k 0.5 q_k U(b_k,c),  init = alpha*U(a,c) - cs[c] | 0
+// q_k = P_k (FIXED) or P_k + beta (U_a.U_b - b_k) (!FIXED); !FIXED also
+// accumulates over upper entries (each constraint once):
 //   sums[0] += p r, sums[1] += r^2, sums[2] += q (r + b).
-// epi(a, h, u_own) is called warp-uniformly; lanes >= s carry junk.
-template <int S, bool FIXED, class Epi>
-__device__ __forceinline__ void row_pass(Ctx& c, const Params& P, const double* __restrict__ U, int s_rt,
-                         const double* __restrict__ Pup, const double* __restrict__ Plo,
-                         double beta, double alpha, const double* cs, bool zero_init,
-                         double (&sums)[3], Epi& epi) {
+// epi(a, c, h, U(a,c)) is called once per (row, column).
+struct UPlain {
+  const double* __restrict__ U;
+  __device__ __forceinline__ double operator()(int64_t o) const { return U[o]; }
+};
+struct UScaled {  // Lanczos: v = src / scale, materialised on the fly
+  const double* __restrict__ src;
+  double sc;
+  __device__ __forceinline__ double operator()(int64_t o) const { return src[o] / sc; }
+};
+
+__device__ __forceinline__ void group_sync(int g) {
+  asm volatile("bar.sync %0, %1;" ::"r"(1 + g), "r"(kGT) : "memory");
+}
+
+template <int S, bool FIXED, class UA, class Epi>
+__device__ __forceinline__ void row_pass_t(Ctx& c, const Params& P, const UA& U, int s_rt,
+                                           const double* __restrict__ Pup,
+                                           const double* __restrict__ Plo, double beta,
+                                           double alpha, const double* cs, bool zero_init,
+                                           double (&sums)[3], Epi& epi) {
   const DevPairs& I = P.I;
   constexpr int SR = S > 0 ? S : kSMax;
+  constexpr int kPer = S > 0 ? kTileEntries / kGT : 1;  // entries per thread per batch
   const int s = S > 0 ? S : s_rt;
-  const int lane = c.lane;
-  double* tile = c.tile;
-  for (int64_t a = c.rl + c.warp; a < c.rh; a += kWarps) {
-    double ua[SR];
-#pragma unroll
-    for (int k = 0; k < SR; ++k) ua[k] = (k < s) ? U[a * s + k] : 0.0;
-    const double uown = lane < s ? U[a * s + lane] : 0.0;
-    double acc = 0.0;
-    if (lane < s && !zero_init) {
-      acc = alpha * uown;
-      if (cs) acc = acc - cs[lane];
+  const int g = threadIdx.x / kGT;   // tile group
+  const int gt = threadIdx.x % kGT;  // thread within the group
+  // double-buffered row pointers (tile t and t + kGroups)
+  int64_t* const vlo0 = c.vlo + g * 2 * (kTileRows + 1);
+  int64_t* const vup0 = c.vup + g * 2 * (kTileRows + 1);
+  double* const tw = c.tw + g * kTileEntries;
+  int32_t* const tcol = c.tcol + g * kTileEntries;
+  double* const tterm = c.tterm + g * 4 * kTileEntries;
+  const int nthr = (kGT / s) * s;  // phase-3 threads of the group; column = gt % s
+  const int mycol = gt % s;
+
+  auto vlo = [&](int buf) { return vlo0 + buf * (kTileRows + 1); };
+  auto vup = [&](int buf) { return vup0 + buf * (kTileRows + 1); };
+  // row pointers of `tile` -> buffer `buf` (visible after the next group_sync)
+  auto load_ptrs = [&](int64_t tile, int buf) {
+    if (tile < c.th) {
+      const int64_t q0 = __ldg(I.tile_row + tile), q1 = __ldg(I.tile_row + tile + 1);
+      if (gt <= (int)(q1 - q0)) {
+        vlo(buf)[gt] = __ldg(I.lo_ptr + q0 + gt);
+        vup(buf)[gt] = __ldg(I.up_ptr + q0 + gt);
+      }
     }
-    const int64_t lo0 = I.lo_ptr[a], nlo = I.lo_ptr[a + 1] - lo0;
-    const int64_t up0 = I.up_ptr[a], nup = I.up_ptr[a + 1] - up0;
-    const int64_t tot = nlo + nup;
-    for (int64_t base = 0; base < tot; base += 32) {
-      const int64_t e = base + lane;
-      const bool valid = e < tot;
-      const bool upper = e >= nlo;
-      int64_t b = 0;
-      double pq = 0.0, bb = 0.0;
-      if (valid) {
-        if (!upper) {
-          b = I.lo_col[lo0 + e];
-          pq = Plo[lo0 + e];
-          if (!FIXED && I.b_lo) bb = I.b_lo[lo0 + e];
-        } else {
-          const int64_t k = up0 + (e - nlo);
-          b = I.ej[k];
-          pq = Pup[k];
-          if (!FIXED && I.b_up) bb = I.b_up[k];
+  };
+  auto tile_nv = [&](int buf, int nr) -> int {
+    return (int)((vlo(buf)[nr] - vlo(buf)[0]) + (vup(buf)[nr] - vup(buf)[0]));
+  };
+
+  // One batch of a thread's entries: indices -> stream loads -> gathers.
+  struct Batch {
+    int64_t bcol[kPer];
+    double pq[kPer], bb[kPer];
+    double ub[kPer][SR];
+    int rowr[kPer];
+    bool ok[kPer], up[kPer];
+  };
+  auto issue = [&](Batch& B, int buf, int nr, int nv, int vb0) {
+    const int64_t* lo = vlo(buf);
+    const int64_t* uq = vup(buf);
+    const int64_t lo0 = lo[0], up0 = uq[0];
+    int64_t idxs[kPer];
+#pragma unroll
+    for (int e = 0; e < kPer; ++e) {
+      const int v = vb0 + gt + e * kGT;
+      B.ok[e] = v < nv;
+      int l = 0, h = nr - 1;  // last row with vstart(r) <= v
+      while (l < h) {
+        const int mid = (l + h + 1) >> 1;
+        const int64_t vs = (lo[mid] - lo0) + (uq[mid] - up0);
+        if (vs <= v) l = mid; else h = mid - 1;
+      }
+      B.rowr[e] = l;
+      const int64_t off = v - ((lo[l] - lo0) + (uq[l] - up0));
+      const int64_t nlo_r = lo[l + 1] - lo[l];
+      B.up[e] = off >= nlo_r;
+      idxs[e] = B.ok[e] ? (B.up[e] ? uq[l] + (off - nlo_r) : lo[l] + off) : 0;
+    }
+#pragma unroll
+    for (int e = 0; e < kPer; ++e) {
+      const int32_t* cp = (B.up[e] ? I.ej : I.lo_col) + idxs[e];
+      const double* pp = (B.up[e] ? Pup : Plo) + idxs[e];
+      const double* bp = B.up[e] ? I.b_up : I.b_lo;
+      B.bcol[e] = __ldg(cp);
+      B.pq[e] = __ldg(pp);
+      B.bb[e] = (!FIXED && bp) ? __ldg(bp + idxs[e]) : 0.0;
+    }
+#pragma unroll
+    for (int e = 0; e < kPer; ++e)
+#pragma unroll
+      for (int k = 0; k < SR; ++k) B.ub[e][k] = (B.ok[e] && k < s) ? U(B.bcol[e] * s + k) : 0.0;
+  };
+  // products w_v U(b_v, c) of a batch -> smem (after the previous fold)
+  auto finish = [&](Batch& B, int64_t r0, int vb0) {
+#pragma unroll
+    for (int e = 0; e < kPer; ++e) {
+      if (!B.ok[e]) continue;
+      const int v = vb0 + gt + e * kGT;
+      double w;
+      if (FIXED) {
+        w = 0.5 * B.pq[e];
+      } else {
+        const int64_t a = r0 + B.rowr[e];
+        double d = 0.0;
+#pragma unroll
+        for (int k = 0; k < SR; ++k)
+          if (k < s) {
+            const double t = U(a * s + k) * B.ub[e][k];
+            d = (k == 0) ? t : d + t;
+          }
+        const double rr = d - B.bb[e];
+        const double q = B.pq[e] + beta * rr;
+        w = 0.5 * q;
+        if (B.up[e]) {
+          sums[0] = sums[0] + B.pq[e] * rr;
+          sums[1] = sums[1] + rr * rr;
+          sums[2] = sums[2] + q * (rr + B.bb[e]);
         }
       }
-      double ub[SR];
+      tw[v] = w;
+      tcol[v] = (int32_t)B.bcol[e];
+      // skipped terms (w == 0, instances.cpp:47) become -0.0: x + (-0.0) == x
+      // exactly, so the fold is branch-free and still bit-identical
 #pragma unroll
-      for (int k = 0; k < SR; ++k) ub[k] = (valid && k < s) ? U[b * s + k] : 0.0;
-      double w = 0.0;
-      if (valid) {
+      for (int k = 0; k < 4; ++k)
+        if (k < s) tterm[v * 4 + k] = (w != 0.0) ? w * B.ub[e][k] : -0.0;
+    }
+  };
+  // phase 3: fold + epilogue, thread per (row, column)
+  auto fold = [&](int buf, int64_t r0, int nr) {
+    const int64_t* lo = vlo(buf);
+    const int64_t* uq = vup(buf);
+    const int64_t lo0 = lo[0], up0 = uq[0];
+    if (gt < nthr) {
+      for (int idx = gt; idx < nr * s; idx += nthr) {
+        const int r = idx / s;
+        const int64_t a = r0 + r;
+        const double uown = U(a * s + mycol);
+        double acc = 0.0;
+        if (!zero_init) {
+          acc = alpha * uown;
+          if (cs) acc = acc - cs[mycol];
+        }
+        const int vb = (int)((lo[r] - lo0) + (uq[r] - up0));
+        const int ve = (int)((lo[r + 1] - lo0) + (uq[r + 1] - up0));
+        if (mycol < 4) {
+          int v = vb;
+          for (; v + 4 <= ve; v += 4) {
+            const double t0 = tterm[v * 4 + mycol], t1 = tterm[(v + 1) * 4 + mycol];
+            const double t2 = tterm[(v + 2) * 4 + mycol], t3 = tterm[(v + 3) * 4 + mycol];
+            acc = acc + t0;
+            acc = acc + t1;
+            acc = acc + t2;
+            acc = acc + t3;
+          }
+          for (; v < ve; ++v) acc = acc + tterm[v * 4 + mycol];
+        } else {
+          for (int v = vb; v < ve; ++v) {
+            const double w = tw[v];
+            if (w != 0.0) acc = acc + w * U((int64_t)tcol[v] * s + mycol);
+          }
+        }
+        epi(a, mycol, acc, uown);
+      }
+    }
+  };
+  // a single row longer than a tile: chunked, fold carried in registers
+  auto long_row = [&](int buf, int64_t a, int nv) {
+    const int64_t* lo = vlo(buf);
+    const int64_t* uq = vup(buf);
+    const int64_t nlo_r = lo[1] - lo[0];
+    double acc = 0.0, uown = 0.0;
+    if (gt < s) {
+      uown = U(a * s + gt);
+      if (!zero_init) {
+        acc = alpha * uown;
+        if (cs) acc = acc - cs[gt];
+      }
+    }
+    for (int v0 = 0; v0 < nv; v0 += kTileEntries) {
+      const int cnt = min(kTileEntries, nv - v0);
+      for (int v = gt; v < cnt; v += kGT) {
+        const int64_t off = v0 + v;
+        const bool upper = off >= nlo_r;
+        const int64_t idx = upper ? uq[0] + (off - nlo_r) : lo[0] + off;
+        const int64_t b = upper ? I.ej[idx] : I.lo_col[idx];
+        const double pq = upper ? Pup[idx] : Plo[idx];
+        double w;
         if (FIXED) {
           w = 0.5 * pq;
         } else {
-          double d = ua[0] * ub[0];
-#pragma unroll
-          for (int k = 1; k < SR; ++k)
-            if (k < s) d = d + ua[k] * ub[k];
-          const double r = d - bb;
-          const double q = pq + beta * r;
+          const double bb = upper ? (I.b_up ? I.b_up[idx] : 0.0) : (I.b_lo ? I.b_lo[idx] : 0.0);
+          double d = 0.0;
+          for (int k = 0; k < s; ++k) {
+            const double t = U(a * s + k) * U(b * s + k);
+            d = (k == 0) ? t : d + t;
+          }
+          const double rr = d - bb;
+          const double q = pq + beta * rr;
           w = 0.5 * q;
           if (upper) {
-            sums[0] = sums[0] + pq * r;
-            sums[1] = sums[1] + r * r;
-            sums[2] = sums[2] + q * (r + bb);
+            sums[0] = sums[0] + pq * rr;
+            sums[1] = sums[1] + rr * rr;
+            sums[2] = sums[2] + q * (rr + bb);
           }
         }
+        tw[v] = w;
+        tcol[v] = (int32_t)b;
       }
-      const unsigned skip = __ballot_sync(kFull, !valid || w == 0.0);
-      const int cnt = (int)min((int64_t)32, tot - base);
-      for (int c0 = 0; c0 < s; c0 += kTile) {
-#pragma unroll
-        for (int t = 0; t < kTile; ++t) {
-          double ubt = 0.0;
-#pragma unroll
-          for (int k = 0; k < SR; ++k)
-            if (k == c0 + t) ubt = ub[k];
-          if (c0 + t < s) tile[t * kTileLd + lane] = w * ubt;
+      group_sync(g);
+      if (gt < s)
+        for (int v = 0; v < cnt; ++v) {
+          const double w = tw[v];
+          if (w != 0.0) acc = acc + w * U((int64_t)tcol[v] * s + gt);
         }
-        __syncwarp();
-        const int cl = lane - c0;
-        if (cl >= 0 && cl < kTile && lane < s) {
-          const double* tc = tile + cl * kTileLd;
-          for (int j = 0; j < cnt; ++j)
-            if (!((skip >> j) & 1u)) acc = acc + tc[j];
-        }
-        __syncwarp();
-      }
+      group_sync(g);
     }
-    epi(a, acc, uown);
+    if (gt < s && gt < nthr) epi(a, gt, acc, uown);
+  };
+
+  // ---- the group's tiles: phase 2 (batched loads/gathers -> smem products,
+  //      next tile's row pointers prefetched into the other buffer), then
+  //      phase 3 (fold + epilogue).  Four groups per CTA overlap their
+  //      latency chains.  (Holding the next tile's batch in registers across
+  //      the fold was measured: ~1 KB of spills per thread, slower.)
+  int64_t t = c.tl + g;
+  int cur = 0;
+  load_ptrs(t, cur);
+  group_sync(g);
+  while (t < c.th) {
+    const int64_t r0 = __ldg(I.tile_row + t);
+    const int nr = (int)(__ldg(I.tile_row + t + 1) - r0);
+    const int nv = tile_nv(cur, nr);
+    if (nv > kTileEntries) {
+      long_row(cur, r0, nv);
+      load_ptrs(t + kGroups, cur ^ 1);
+      group_sync(g);
+    } else {
+      for (int vb0 = 0; vb0 < nv; vb0 += kPer * kGT) {  // one round unless S == 0
+        Batch B;
+        issue(B, cur, nr, nv, vb0);
+        finish(B, r0, vb0);
+      }
+      load_ptrs(t + kGroups, cur ^ 1);
+      group_sync(g);
+      fold(cur, r0, nr);
+      group_sync(g);
+    }
+    t += kGroups;
+    cur ^= 1;
   }
+  __syncthreads();
+}
+
+template <int S, bool FIXED, class Epi>
+__device__ __forceinline__ void row_pass(Ctx& c, const Params& P, const double* __restrict__ U,
+                                         int s_rt, const double* __restrict__ Pup,
+                                         const double* __restrict__ Plo, double beta, double alpha,
+                                         const double* cs, bool zero_init, double (&sums)[3],
+                                         Epi& epi) {
+  row_pass_t<S, FIXED>(c, P, UPlain{U}, s_rt, Pup, Plo, beta, alpha, cs, zero_init, sums, epi);
+}
+
+// Stage per-thread column partials (in each 128-thread group, thread
+// gt < (kGT/s)*s owns column gt % s) into rs.part[w][base + c] as per-warp sums in fixed order, for a
+// following team_reduce_smem.  Uses the tile smem as scratch (call after a pass).
+__device__ __forceinline__ void stage_colsums(Ctx& c, int s, int base, double val) {
+  double* scr = c.tw;
+  const int tid = threadIdx.x;
+  const int nthr = (kGT / s) * s;
+  const int gt = tid % kGT;
+  scr[tid] = gt < nthr ? val : 0.0;
+  __syncthreads();
+  if (c.lane < s) {
+    double acc = 0.0;
+    for (int l = 0; l < 32; ++l) {
+      const int t = c.warp * 32 + l;
+      const int tg = t % kGT;
+      if (tg < nthr && tg % s == c.lane) acc = acc + scr[t];
+    }
+    c.rs.part[c.warp * kRedK + base + c.lane] = acc;
+  }
+  __syncthreads();
 }
 
 // GradientOperator build (sdp_instance.cpp:73-83): for every pair constraint
@@ -563,16 +779,14 @@ __device__ __noinline__ bool fista_dev(Ctx& c, const Params& P, Roles& R, int s,
       double nrmz;
       {
         double hU = 0.0, zz = 0.0;
-        auto epi = [&](int64_t row, double h, double xo) {
-          if (c.lane < s) {
-            const int64_t o = row * s + c.lane;
-            hU = hU + h * xo;
-            const double g = 2.0 * h;
-            const double gt = lambda * g + (xo - W[o]);
-            GT[o] = gt;
-            const double z = xo - gt / L;
-            zz = zz + z * z;
-          }
+        auto epi = [&](int64_t row, int cc, double h, double xo) {
+          const int64_t o = row * s + cc;
+          hU = hU + h * xo;
+          const double g = 2.0 * h;
+          const double gt = lambda * g + (xo - W[o]);
+          GT[o] = gt;
+          const double z = xo - gt / L;
+          zz = zz + z * z;
         };
         double sums[3] = {0.0, 0.0, 0.0};
         row_pass<S, false>(c, P, XT, s, P.p_up, P.p_lo, beta, theta_alpha_or_half(I, qt),
@@ -690,9 +904,9 @@ __device__ __noinline__ bool fista_dev(Ctx& c, const Params& P, Roles& R, int s,
       const double Lm = L - mu, mua = mu * a, tam = tau - a * mu;
       const double an = fista_a(tau, A_next, L, mu);
       double vv = 0.0, ddn = 0.0, ntn = 0.0, csn = 0.0;
-      auto epi = [&](int64_t row, double h, double yo) {
-        if (c.lane < s) {
-          const int64_t o = row * s + c.lane;
+      auto epi = [&](int64_t row, int cc, double h, double yo) {
+        {
+          const int64_t o = row * s + cc;
           const double g = 2.0 * h;
           const double gy = lambda * g + (yo - W[o]);
           const double xt = XT[o];
@@ -715,7 +929,7 @@ __device__ __noinline__ bool fista_dev(Ctx& c, const Params& P, Roles& R, int s,
                          theta ? c.cs : nullptr, false, sums, epi);
       double v[3] = {vv, ddn, ntn};
       stage_scalars<3>(c, v);
-      if (c.lane < s) c.rs.part[c.warp * kRedK + 3 + c.lane] = csn;
+      stage_colsums(c, s, 3, csn);
       team_reduce_smem(c.t, c.rs, 3 + s);
       prof_mark(c, P, kPfT5);
       vv = c.rs.out[0];

@@ -298,9 +298,7 @@ __device__ __noinline__ void op_dispatch(Ctx& c, const Params& P, SolveOut* so) 
       factor_stats<S>(c, P, U, s, &nrm2);
       const bool withC = P.op == kOpCPlusAdj;
       double* out = P.out_mat;
-      auto epi = [&](int64_t a, double h, double) {
-        if (c.lane < s) out[a * s + c.lane] = h;
-      };
+      auto epi = [&](int64_t a, int cc, double h, double) { out[a * s + cc] = h; };
       double sums[3] = {0, 0, 0};
       const double alpha = is_theta(I) ? P.q_trace_in : 0.5;
       const bool zero = !is_theta(I) && !withC;
@@ -335,13 +333,11 @@ __device__ __noinline__ void op_dispatch(Ctx& c, const Params& P, SolveOut* so) 
       }
       double hU = 0.0, bad = 0.0;
       double* out = P.out_mat;
-      auto epi = [&](int64_t a, double h, double uo) {
-        if (c.lane < s) {
-          hU = hU + h * uo;
-          const double g = 2.0 * h;
-          if (!isfinite(g)) bad = 1.0;
-          out[a * s + c.lane] = g;
-        }
+      auto epi = [&](int64_t a, int cc, double h, double uo) {
+        hU = hU + h * uo;
+        const double g = 2.0 * h;
+        if (!isfinite(g)) bad = 1.0;
+        out[a * s + cc] = g;
       };
       double sums[3] = {0, 0, 0};
       row_pass<S, false>(c, P, U, s, P.p_up, P.p_lo, beta, theta_alpha_or_half(I, qt),
@@ -423,11 +419,9 @@ __device__ __noinline__ void op_dispatch(Ctx& c, const Params& P, SolveOut* so) 
           }
           case 2: {  // fused value + gradient row pass (FISTA T2 / T5 shape)
             double hU = 0.0;
-            auto epi = [&](int64_t a, double h, double uo) {
-              if (c.lane < s) {
-                hU = hU + h * uo;
-                out[a * s + c.lane] = 2.0 * h;
-              }
+            auto epi = [&](int64_t a, int cc, double h, double uo) {
+              hU = hU + h * uo;
+              out[a * s + cc] = 2.0 * h;
             };
             double sums[3] = {0, 0, 0};
             row_pass<S, false>(c, P, U, s, P.p_up, P.p_lo, beta, theta_alpha_or_half(I, qt),
@@ -443,9 +437,7 @@ __device__ __noinline__ void op_dispatch(Ctx& c, const Params& P, SolveOut* so) 
             break;
           }
           case 4: {  // Lanczos matvec: fixed-q adjoint at s = 1 on column 0
-            auto epi = [&](int64_t a, double h, double) {
-              if (c.lane == 0) out[a] = -h;
-            };
+            auto epi = [&](int64_t a, int, double h, double) { out[a] = -h; };
             double sums[3] = {0, 0, 0};
             row_pass<1, true>(c, P, U, 1, P.p_up, P.p_lo, 0.0, theta_alpha_or_half(I, qt),
                               is_theta(I) ? c.cs : nullptr, false, sums, epi);

@@ -179,54 +179,18 @@ struct Pending {
 // (apply_B, lanczos.cpp:38); also writes v into slot pend.dst for own rows.
 // The caller has team-synchronised after pend.src was written.
 __device__ __forceinline__ void lz_apply(Ctx& c, const Params& P, const GOp& g, const Pending& pv,
-                                      double* out) {
+                                         double* out) {
   const DevPairs& I = P.I;
-  const int64_t n = I.n;
-  (void)n;
-  const double* src = pv.src;
-  const double sc = pv.scale;
   double* vdst = pv.dst >= 0 ? slot_ptr(P, pv.dst) : nullptr;
-  const double alpha = theta_alpha_or_half(I, g.qt);
-  const bool theta = is_theta(I);
-  const int lane = c.lane;
-  double* tile = c.tile;
-  for (int64_t a = c.rl + c.warp; a < c.rh; a += kWarps) {
-    const double va = src[a] / sc;
-    if (vdst && lane == 0) vdst[a] = va;
-    double acc = alpha * va;
-    if (theta) acc = acc - pv.sum;
-    const int64_t lo0 = I.lo_ptr[a], nlo = I.lo_ptr[a + 1] - lo0;
-    const int64_t up0 = I.up_ptr[a], nup = I.up_ptr[a + 1] - up0;
-    const int64_t tot = nlo + nup;
-    for (int64_t base = 0; base < tot; base += 32) {
-      const int64_t e = base + lane;
-      const bool valid = e < tot;
-      double w = 0.0, vb = 0.0;
-      if (valid) {
-        int64_t b;
-        if (e < nlo) {
-          b = I.lo_col[lo0 + e];
-          w = 0.5 * g.qlo[lo0 + e];
-        } else {
-          const int64_t k = up0 + (e - nlo);
-          b = I.ej[k];
-          w = 0.5 * g.qup[k];
-        }
-        vb = src[b] / sc;
-      }
-      const unsigned skip = __ballot_sync(kFull, !valid || w == 0.0);
-      tile[lane] = w * vb;
-      __syncwarp();
-      if (lane == 0) {
-        const int cnt = (int)min((int64_t)32, tot - base);
-        for (int j = 0; j < cnt; ++j)
-          if (!((skip >> j) & 1u)) acc = acc + tile[j];
-      }
-      __syncwarp();
-    }
-    if (lane == 0) out[a] = -acc;
-  }
-  __syncthreads();
+  auto epi = [&](int64_t a, int, double h, double va) {
+    out[a] = -h;
+    if (vdst) vdst[a] = va;
+  };
+  double sums[3] = {0.0, 0.0, 0.0};
+  const double sumv = pv.sum;
+  row_pass_t<1, true>(c, P, UScaled{pv.src, pv.scale}, 1, g.qup, g.qlo, 0.0,
+                      theta_alpha_or_half(I, g.qt), is_theta(I) ? &sumv : nullptr, false, sums,
+                      epi);
 }
 
 // sum_i V_i(a) e_i in increasing i, with the loads issued in batches of 8
@@ -593,9 +557,7 @@ __device__ __noinline__ double fw_gap_dev(Ctx& c, const Params& P, const double*
   double ny2;
   factor_stats<S>(c, P, Y, s, &ny2);
   double gs = 0.0;
-  auto epi = [&](int64_t, double h, double yo) {
-    if (c.lane < s) gs = gs + h * yo;
-  };
+  auto epi = [&](int64_t, int, double h, double yo) { gs = gs + h * yo; };
   double sums[3] = {0.0, 0.0, 0.0};
   row_pass<S, true>(c, P, Y, s, g.qup, g.qlo, 0.0, theta_alpha_or_half(I, g.qt),
                     is_theta(I) ? c.cs : nullptr, false, sums, epi);

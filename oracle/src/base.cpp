@@ -62,8 +62,10 @@ bool all_finite(const Vec& v) {
 // Tournament (circle-method) ordering: k' = k rounded up to even; in round r
 // player positions rotate with player 0 fixed.  Within a round all pair
 // rotations are applied to rows first, then to columns, then the pivots are
-// zeroed.  The device eigensolver (csrc/solver_device.cuh) performs the same
-// floating-point operations in the same order.
+// zeroed.  The device eigensolver (csrc/solver.cuh jacobi_dev) uses the same
+// rotation schedule and formulas with a looser stopping threshold (2 ulp of
+// the largest entry); this checker keeps the tight one (over-converged, like
+// Eigen's full-precision SelfAdjointEigenSolver).
 void jacobi_eigh(int k, const double* H, double* evals, double* evecs) {
   std::vector<double> A(H, H + size_t(k) * k);
   std::vector<double> V(static_cast<size_t>(k) * k, 0.0);

@@ -178,6 +178,19 @@ typedef struct cuhallar_solution cuhallar_solution;
 int cuhallar_solve(cuhallar_instance* inst, const cuhallar_config* cfg, const double* U0_host,
                    int s0, const double* p0_host, cuhallar_report* rep,
                    cuhallar_solution** sol, cuhallar_trace_fn fn, void* user);
+/* Row-sharded solve over `world` ranks (no reference
+ * counterpart — the reference is single-process, solver.hpp:95-101 is the
+ * interface it extends).  insts[r] is the same instance built on rank r's
+ * device (e.g. one per B200); each rank's persistent launch owns a contiguous
+ * block of rows and the upper constraints of those rows, pushes the rows of
+ * every gathered factor into its peers' replicas over peer memory
+ * (NVLink/NVSwitch), and joins the per-rank partial sums of every reduction
+ * in rank order.  Ranks may share a device (co-resident launches, used by the
+ * single-GPU tests).  Pair families only (theta, matrix completion); the
+ * report's device_seconds is the max over ranks. */
+int cuhallar_solve_sharded(cuhallar_instance* const* insts, int world, const cuhallar_config* cfg,
+                           const double* U0_host, int s0, const double* p0_host,
+                           cuhallar_report* rep, cuhallar_solution** sol);
 /* SolveReport::U (n x rank, column-major) and SolveReport::dual.p (length m) */
 int cuhallar_solution_get_U(const cuhallar_solution* sol, double* U_host);
 int cuhallar_solution_get_p(const cuhallar_solution* sol, double* p_host);

@@ -202,6 +202,17 @@ class SdpInstance:
         _check(_lib.cuhallar_instance_get_pairs(self._h, i.ctypes.data_as(_i64p), j.ctypes.data_as(_i64p)))
         return i, j
 
+    def pr_data(self):
+        """PrInstance::hidden_x (nc) and masks (nc x L) of a phase-retrieval instance."""
+        if self.kind != "phaseret":
+            raise InputError("pr_data: not a phase-retrieval instance")
+        nc = self.n // 2
+        L = self.m // nc
+        x = np.empty(nc, dtype=np.complex128)
+        masks = np.empty(nc * L, dtype=np.complex128)
+        _check(_lib.cuhallar_instance_get_phaseret(self._h, x.ctypes.data_as(_dp), masks.ctypes.data_as(_dp)))
+        return x, masks.reshape(L, nc).T
+
     # -- operator callables; U is n x s (numpy or torch), results numpy --
     def _dev_factor(self, U):
         import torch
@@ -504,15 +515,44 @@ def solve(inst: SdpInstance, cfg: SolverConfig = None, U0=None, p0=None,
                                  e.rank, e.al_value, e.fw_alpha, e.rel_pfeas, e.rel_gap, e.rel_dfeas))
 
     cb = _TRACE_FN(_cb) if sink is not None else _TRACE_FN()
-    if U0 is not None:
-        U0a = np.asfortranarray(np.asarray(U0, dtype=np.float64).reshape(inst.n, -1))
-        p0a = np.ascontiguousarray(p0 if p0 is not None else np.zeros(inst.m), dtype=np.float64)
-        rc = _lib.cuhallar_solve(inst._h, C.byref(cc), U0a.ctypes.data_as(_dp), C.c_int(U0a.shape[1]),
-                                 p0a.ctypes.data_as(_dp), C.byref(rep), C.byref(sol), cb, None)
-    else:
-        rc = _lib.cuhallar_solve(inst._h, C.byref(cc), None, C.c_int(0), None, C.byref(rep),
-                                 C.byref(sol), cb, None)
+    U0p, s0, p0p, _keep = _start_args(inst, U0, p0)
+    rc = _lib.cuhallar_solve(inst._h, C.byref(cc), U0p, C.c_int(s0), p0p, C.byref(rep), C.byref(sol),
+                             cb, None)
     _check(rc)
+    r = _report(inst, rep, sol, fetch)
+    if sink is not None:
+        for e in events:
+            sink(e)
+        r.trace = events
+    return r
+
+
+def _start_args(inst, U0, p0):
+    if U0 is None:
+        return None, 0, None, None
+    U0a = np.asfortranarray(np.asarray(U0, dtype=np.float64).reshape(inst.n, -1))
+    p0a = np.ascontiguousarray(p0 if p0 is not None else np.zeros(inst.m), dtype=np.float64)
+    return U0a.ctypes.data_as(_dp), U0a.shape[1], p0a.ctypes.data_as(_dp), (U0a, p0a)
+
+
+def solve_sharded(insts, cfg: SolverConfig = None, U0=None, p0=None, fetch: bool = True) -> SolveReport:
+    """Row-sharded solve: ``insts[r]`` is the same instance built
+    on rank r's device (``with torch.cuda.device(r): build(...)``).  Each rank's
+    persistent launch owns a block of rows; gathered factor rows travel over
+    peer memory and reductions join per-rank partials in rank order.  Ranks may
+    share one device (co-resident launches).  Theta and matrix completion only."""
+    cfg = cfg or SolverConfig()
+    cc = cfg._c()
+    rep = CReport()
+    sol = C.c_void_p()
+    arr = (C.c_void_p * len(insts))(*[i._h for i in insts])
+    U0p, s0, p0p, _keep = _start_args(insts[0], U0, p0)
+    _check(_lib.cuhallar_solve_sharded(arr, C.c_int(len(insts)), C.byref(cc), U0p, C.c_int(s0), p0p,
+                                       C.byref(rep), C.byref(sol)))
+    return _report(insts[0], rep, sol, fetch)
+
+
+def _report(inst, rep, sol, fetch) -> SolveReport:
     try:
         r = SolveReport(status=STATUS[rep.status], pval=rep.pval, dval=rep.dval,
                         dval_no_theta=rep.dval_no_theta, rel_pfeas=rep.rel_pfeas, rel_gap=rep.rel_gap,
@@ -530,8 +570,4 @@ def solve(inst: SdpInstance, cfg: SolverConfig = None, U0=None, p0=None,
             r.p = p
     finally:
         _lib.cuhallar_solution_destroy(sol)
-    if sink is not None:
-        for e in events:
-            sink(e)
-        r.trace = events
     return r

@@ -25,8 +25,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     hallar_kernel(const __grid_constant__ Params P, SolveOut* so) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Ctx c;
-  c.t.rank = blockIdx.x;
-  c.t.size = gridDim.x;
+  c.t.rank = P.fab.me * gridDim.x + blockIdx.x;  // global CTA index over all ranks
+  c.t.size = P.fab.world * gridDim.x;
+  c.t.lrank = blockIdx.x;
+  c.t.lsize = gridDim.x;
+  c.t.fab = &P.fab;
   c.t.bar = P.bar;
   c.t.slots = P.slots;
   c.t.epoch = 0;
@@ -38,16 +41,21 @@ __global__ void __launch_bounds__(kThreads, 1)
   sm += kWarps * kRedK;
   c.rs.out = sm;
   sm += kRedK;
-  c.tw = sm;
-  sm += kGroups * kTileEntries;
-  c.tterm = sm;
-  sm += kGroups * 4 * kTileEntries;
-  c.vlo = reinterpret_cast<int64_t*>(sm);
-  sm += 2 * kGroups * (kTileRows + 1);
-  c.vup = reinterpret_cast<int64_t*>(sm);
-  sm += 2 * kGroups * (kTileRows + 1);
-  c.tcol = reinterpret_cast<int32_t*>(sm);
-  sm += kGroups * kTileEntries / 2;
+  {
+    // one pass scratch: tile-engine arrays, or the phase-retrieval transform
+    double* base = sm;
+    c.X = reinterpret_cast<double2*>(base);
+    c.tw = sm;
+    sm += kGroups * kTileEntries;
+    c.tterm = sm;
+    sm += kGroups * 4 * kTileEntries;
+    c.vlo = reinterpret_cast<int64_t*>(sm);
+    sm += 2 * kGroups * (kTileRows + 1);
+    c.vup = reinterpret_cast<int64_t*>(sm);
+    sm += 2 * kGroups * (kTileRows + 1);
+    c.tcol = reinterpret_cast<int32_t*>(sm);
+    sm = base + kPassScratch;
+  }
   c.cs = sm;
   sm += 2 * kSMax;
   c.H = sm;
@@ -72,12 +80,24 @@ __global__ void __launch_bounds__(kThreads, 1)
   c.col = ip;
   ip += 40;
   c.jpq = ip;
-  c.tl = P.I.ntiles * c.t.rank / c.t.size;
-  c.th = P.I.ntiles * (c.t.rank + 1) / c.t.size;
-  c.rl = P.I.tile_row[c.tl];
-  c.rh = P.I.tile_row[c.th];
-  c.kl = P.I.np * c.t.rank / c.t.size;
-  c.kh = P.I.np * (c.t.rank + 1) / c.t.size;
+  if (P.I.family == kPhaseret) {
+    c.tl = c.th = 0;
+    c.rl = P.I.n * c.t.rank / c.t.size;
+    c.rh = P.I.n * (c.t.rank + 1) / c.t.size;
+  } else {
+    c.tl = P.I.ntiles * c.t.rank / c.t.size;
+    c.th = P.I.ntiles * (c.t.rank + 1) / c.t.size;
+    c.rl = P.I.tile_row[c.tl];
+    c.rh = P.I.tile_row[c.th];
+  }
+  if (P.fab.world > 1) {
+    // row-owner sharding: a CTA owns the upper (edge-order) entries of its rows
+    c.kl = P.I.up_ptr[c.rl];
+    c.kh = P.I.up_ptr[c.rh];
+  } else {
+    c.kl = P.I.np * c.t.rank / c.t.size;
+    c.kh = P.I.np * (c.t.rank + 1) / c.t.size;
+  }
   if (P.op == kOpSolve) {
     solve_dev(c, P, so);
   } else {
@@ -113,9 +133,7 @@ namespace {
 thread_local std::string g_err;
 
 constexpr size_t kSmemBytes =
-    sizeof(double) * (kWarps * kRedK + kRedK + kGroups * (5 * kTileEntries + 4 * (kTileRows + 1) +
-                                                        kTileEntries / 2) +
-                      2 * kSMax + kHLd * kHLd +
+    sizeof(double) * (kWarps * kRedK + kRedK + kPassScratch + 2 * kSMax + kHLd * kHLd +
                       3 * 32 * 32 + 4 * 32 + 64) +
     sizeof(int) * 80;
 
@@ -143,7 +161,15 @@ T* dupload(const std::vector<T>& v, int64_t* acct) {
 }
 
 int grid_size(int requested) {
-  static int cached = -1;
+  static int cache[64];
+  static bool init = false;
+  if (!init) {
+    for (auto& x : cache) x = -1;
+    init = true;
+  }
+  int cur = 0;
+  ck(cudaGetDevice(&cur), "device");
+  int& cached = cache[cur & 63];
   if (cached < 0) {
     ck(cudaFuncSetAttribute(hallar_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             int(kSmemBytes)),
@@ -174,6 +200,7 @@ struct cuhallar_instance {
   int64_t *up_ptr = nullptr, *lo_ptr = nullptr, *lo_eid = nullptr, *tile_row = nullptr;
   double *b_up = nullptr, *b_lo = nullptr;      // scaled b/tau (solve)
   double *ub_up = nullptr, *ub_lo = nullptr;    // unscaled b (operator ABI), lazy
+  double2 *masks = nullptr, *twid = nullptr, *prF = nullptr, *prG = nullptr;  // phase retrieval
   // workspace
   int ws_grid = 0;
   unsigned long long* bar = nullptr;
@@ -181,6 +208,14 @@ struct cuhallar_instance {
   double* buf[kNBuf] = {};
   double* vslot = nullptr;
   int nslot = 0;
+  double* arena = nullptr;  // buf[0..kNBuf) and the Lanczos slots: the replicated factor arena
+  int64_t arena_len = 0;
+  int device = 0;
+  std::vector<int64_t> tile_row_host, up_ptr_host;
+  // sharded-solve rendezvous state (this rank's side)
+  unsigned long long* xbar = nullptr;
+  double* xslots = nullptr;
+  int* xerr = nullptr;
   double *p_up = nullptr, *p_lo = nullptr, *q_up = nullptr, *q_lo = nullptr, *r_up = nullptr,
          *r_lo = nullptr;
   double* lz_rand = nullptr;
@@ -201,7 +236,8 @@ struct cuhallar_instance {
       if (p) cudaFree(p);
     };
     f(ei); f(ej); f(lo_col); f(up_ptr); f(lo_ptr); f(lo_eid); f(tile_row); f(b_up); f(b_lo); f(ub_up); f(ub_lo);
-    f(bar); f(slots); for (auto* b : buf) f(b); f(vslot);
+    f(masks); f(twid); f(prF); f(prG);
+    f(bar); f(slots); f(arena); f(xbar); f(xslots); f(xerr);
     f(p_up); f(p_lo); f(q_up); f(q_lo); f(r_up); f(r_lo); f(lz_rand); f(dscal); f(discal); f(dso); f(dprof);
     if (trace_host) cudaFreeHost(trace_host);
     if (trace_count_host) cudaFreeHost(trace_count_host);
@@ -273,6 +309,8 @@ void upload_pairs(cuhallar_instance* in) {
       r0 = r1;
     }
     in->tile_row = dupload(tr, &in->bytes);
+    in->tile_row_host = tr;
+    in->up_ptr_host = up;
     in->I.tile_row = in->tile_row;
     in->I.ntiles = int64_t(tr.size()) - 1;
   }
@@ -316,7 +354,13 @@ void ensure_workspace(cuhallar_instance* in, int grid, uint64_t seed, int block_
   const int64_t n = in->h.n, np = in->h.np;
   if (!in->bar) {
     in->bar = dalloc<unsigned long long>(1, &in->bytes);
-    for (auto& b : in->buf) b = dalloc<double>(size_t(n) * kSMax, &in->bytes);
+    // factor pool + Lanczos slots in one allocation, identical layout on every
+    // rank of a sharded solve (peer address = peer arena + same offset)
+    in->nslot = kLanczosMax + kLanczosMax / 3 + 8;
+    in->arena_len = int64_t(n) * (int64_t(kNBuf) * kSMax + in->nslot);
+    in->arena = dalloc<double>(size_t(in->arena_len), &in->bytes);
+    for (int i = 0; i < kNBuf; ++i) in->buf[i] = in->arena + size_t(i) * n * kSMax;
+    in->vslot = in->arena + size_t(kNBuf) * n * kSMax;
     in->p_up = dalloc<double>(np, &in->bytes);
     in->p_lo = dalloc<double>(np, &in->bytes);
     in->q_up = dalloc<double>(np, &in->bytes);
@@ -335,13 +379,7 @@ void ensure_workspace(cuhallar_instance* in, int grid, uint64_t seed, int block_
     in->slots = dalloc<double>(size_t(2) * grid * kRedK, &in->bytes);
     in->ws_grid = grid;
   }
-  const int kmax = int(std::min<int64_t>(block_restart, n));
-  const int need = kmax + std::max(1, kmax / 3) + 8;
-  if (need > in->nslot) {
-    if (in->vslot) cudaFree(in->vslot);
-    in->vslot = dalloc<double>(size_t(n) * need, &in->bytes);
-    in->nslot = need;
-  }
+  (void)block_restart;  // slots sized for the device cap (kLanczosMax) at allocation
   if (seed != in->lz_seed) {
     // Lanczos start vector + breakdown refills: the stream of
     // gaussian_vector(n, Rng(seed ^ 0x9b97f4a7c15)) calls (lanczos.cpp:46-50, 128-129)
@@ -353,6 +391,73 @@ void ensure_workspace(cuhallar_instance* in, int grid, uint64_t seed, int block_
     in->n_refill = refill;
     in->lz_seed = seed;
   }
+}
+
+Params base_params(cuhallar_instance* in, const cuhallar_config* cfg);
+int launch(cuhallar_instance* in, Params& P, int grid, cudaStream_t st, SolveOut* so,
+           float* ms = nullptr);
+
+void upload_pr(cuhallar_instance* in) {
+  auto& h = in->h;
+  const int64_t nc = h.nc, m = h.m;
+  h.np = m;  // constraint-order vectors (p, q, r, b) use the edge-order slots
+  int lg = 0;
+  while ((int64_t(1) << lg) < nc) ++lg;
+  {
+    std::vector<double2> mk(h.masks.size()), tw(std::max<size_t>(1, h.twiddle.size()));
+    for (size_t i = 0; i < mk.size(); ++i) mk[i] = make_double2(h.masks[i].real(), h.masks[i].imag());
+    for (size_t i = 0; i < h.twiddle.size(); ++i)
+      tw[i] = make_double2(h.twiddle[i].real(), h.twiddle[i].imag());
+    in->masks = dupload(mk, &in->bytes);
+    in->twid = dupload(tw, &in->bytes);
+  }
+  in->prF = dalloc<double2>(size_t(kSMax) * m, &in->bytes);
+  in->prG = dalloc<double2>(size_t(kSMax) * m, &in->bytes);
+  in->h2d += in->bytes;
+  DevPairs& I = in->I;
+  I.family = kPhaseret;
+  I.has_trace = 0;
+  I.n = h.n;
+  I.np = m;
+  I.m = m;
+  I.nc = nc;
+  I.L = h.L;
+  I.lognc = lg;
+  I.masks = in->masks;
+  I.twid = in->twid;
+  I.F = in->prF;
+  I.G = in->prG;
+  I.norm_C1 = h.norm_C1;
+  // b = A(x x*) of the hidden signal through the device map (s = 1)
+  {
+    const int grid = grid_size(0);
+    ensure_workspace(in, grid, 0, 30);
+    std::vector<double> x(size_t(h.n));
+    for (int64_t j = 0; j < nc; ++j) {
+      x[j] = h.hidden_x[j].real();
+      x[nc + j] = h.hidden_x[j].imag();
+    }
+    ck(cudaMemcpy(in->buf[0], x.data(), x.size() * sizeof(double), cudaMemcpyHostToDevice), "x");
+    double* bd = in->r_up;  // scratch
+    Params P = base_params(in, nullptr);
+    P.op = kOpMap;
+    P.s_in = 1;
+    P.out_vec = bd;
+    SolveOut so{};
+    if (launch(in, P, grid, 0, &so, nullptr) != kOk) throw CudaError("phaseret: b map failed");
+    h.b.resize(m);
+    ck(cudaMemcpy(h.b.data(), bd, m * sizeof(double), cudaMemcpyDeviceToHost), "b");
+  }
+  h.norm_b1 = hh::eigen_order_sum_abs(h.b.data(), m);
+  // scale_instance (solver.cpp:31-42)
+  std::vector<double> bs(m);
+  for (int64_t k = 0; k < m; ++k) bs[k] = h.tau != 1.0 ? h.b[k] / h.tau : h.b[k];
+  I.norm_b1 = h.tau != 1.0 ? h.norm_b1 / h.tau : h.norm_b1;
+  I.nb2 = std::sqrt(hh::eigen_order_sum_sq(bs.data(), m));
+  in->b_up = dupload(bs, &in->bytes);
+  in->h2d += int64_t(m * sizeof(double));
+  I.b_up = in->b_up;
+  I.b_lo = nullptr;
 }
 
 Cfg to_dev_cfg(const cuhallar_config& c) {
@@ -415,6 +520,7 @@ const char* msg_text(int id) {
     case kMsgRankCap: return "factor rank exceeds the device cap (32)";
     case kMsgRefillCap: return "lanczos: breakdown refill / slot capacity exceeded";
     case kMsgRank32: return "factor rank above 32 is not supported";
+    case kMsgFabric: return "sharded solve: a peer rank did not reach the rendezvous (timeout)";
     default: return "";
   }
 }
@@ -459,10 +565,13 @@ Params base_params(cuhallar_instance* in, const cuhallar_config* cfg) {
 void use_unscaled_b(cuhallar_instance* in, Params& P) {
   if (in->h.has_trace || in->h.tau == 1.0) return;
   if (!in->ub_up) {
-    std::vector<double> up(in->h.b.begin(), in->h.b.begin() + in->h.np), lo(in->h.np);
-    for (int64_t e = 0; e < in->h.np; ++e) lo[e] = up[in->lo_eid_host[e]];
+    std::vector<double> up(in->h.b.begin(), in->h.b.begin() + in->h.np);
     in->ub_up = dupload(up, &in->bytes);
-    in->ub_lo = dupload(lo, &in->bytes);
+    if (in->h.family != kPhaseret) {
+      std::vector<double> lo(in->h.np);
+      for (int64_t e = 0; e < in->h.np; ++e) lo[e] = up[in->lo_eid_host[e]];
+      in->ub_lo = dupload(lo, &in->bytes);
+    }
   }
   P.I.b_up = in->ub_up;
   P.I.b_lo = in->ub_lo;
@@ -470,7 +579,7 @@ void use_unscaled_b(cuhallar_instance* in, Params& P) {
 
 // Launch the persistent kernel; returns the solver status and fills *so.
 int launch(cuhallar_instance* in, Params& P, int grid, cudaStream_t st, SolveOut* so,
-           float* ms = nullptr) {
+           float* ms) {
   ck(cudaMemsetAsync(in->bar, 0, sizeof(unsigned long long), st), "memset bar");
   ck(cudaMemsetAsync(in->dso, 0, sizeof(SolveOut), st), "memset out");
   if (in->trace_count_host) *in->trace_count_host = 0;
@@ -504,6 +613,15 @@ int status_to_rc(int st, int msg) {
   return CUHALLAR_ERR_CUDA;
 }
 
+struct DevGuard {  // run an entry point on the instance's device
+  int prev = 0;
+  explicit DevGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DevGuard() { cudaSetDevice(prev); }
+};
+
 template <class F>
 int guard(F&& f) {
   try {
@@ -525,14 +643,24 @@ int guard(F&& f) {
 
 cuhallar_instance* finish_pairs(hh::HostInst&& h) {
   auto in = std::make_unique<cuhallar_instance>();
+  ck(cudaGetDevice(&in->device), "device");
   in->h = std::move(h);
   upload_pairs(in.get());
   return in.release();
 }
 
-void check_pairs(const cuhallar_instance* in) {
-  if (in->h.family == kPhaseret)
-    throw hh::InputError("phase retrieval: device operator path not available in this build");
+void check_pairs(const cuhallar_instance*) {}
+
+// gen_phase_retrieval (instances.cpp:298-389): masks, twiddles and the
+// spectrum / adjoint scratch go to HBM; b = map of the hidden signal is
+// computed by the device operator itself (instances.cpp:323-328).
+void upload_pr(cuhallar_instance* in);
+cuhallar_instance* finish_pr(hh::HostInst&& h) {
+  auto in = std::make_unique<cuhallar_instance>();
+  ck(cudaGetDevice(&in->device), "device");
+  in->h = std::move(h);
+  upload_pr(in.get());
+  return in.release();
 }
 
 // column-major (host or device) U -> buffer 0 (row-major)
@@ -555,8 +683,10 @@ double load_multiplier_dev(cuhallar_instance* in, const double* p_dev, double* u
                            cudaStream_t st) {
   const int64_t np = in->h.np;
   ck(cudaMemcpyAsync(up, p_dev, sizeof(double) * np, cudaMemcpyDeviceToDevice, st), "D2D p");
-  gather_lower<<<unsigned((np + 255) / 256), 256, 0, st>>>(p_dev, in->lo_eid, np, lo);
-  ck(cudaGetLastError(), "gather_lower");
+  if (in->h.family != kPhaseret) {
+    gather_lower<<<unsigned((np + 255) / 256), 256, 0, st>>>(p_dev, in->lo_eid, np, lo);
+    ck(cudaGetLastError(), "gather_lower");
+  }
   double pt = 0.0;
   if (in->h.has_trace)
     ck(cudaMemcpyAsync(&pt, p_dev + np, sizeof(double), cudaMemcpyDeviceToHost, st), "D2H pt");
@@ -645,9 +775,9 @@ int64_t cuhallar_matcomp_constraint_count(int64_t n1, int64_t n2, int r, int off
 int cuhallar_gen_phase_retrieval(int64_t n, int L, uint64_t seed, double tau_slack,
                                  cuhallar_instance** out) {
   return guard([&] {
-    (void)hh::make_phaseret(n, L, seed, tau_slack);
-    throw hh::InputError("phase retrieval: device operator path not available in this build");
-    *out = nullptr;
+    if (n > kPrMaxNc)
+      throw hh::InputError("phaseret: n above the device transform length cap (8192)");
+    *out = finish_pr(hh::make_phaseret(n, L, seed, tau_slack));
     return 0;
   });
 }
@@ -693,6 +823,7 @@ static int run_op(cuhallar_instance* in, int op, const double* U_dev, int64_t ld
                   int64_t ldo, double* val_host, cudaStream_t st) {
   return guard([&] {
     check_pairs(in);
+    DevGuard dg(in->device);
     if (s < 1 || s > kSMax) throw hh::InputError("factor rank must be in [1, 32]");
     if (ldu < in->h.n) throw hh::InputError("leading dimension < n");
     std::lock_guard<std::mutex> lk(in->mu);
@@ -780,11 +911,37 @@ static double host_multiplier_to_dev(cuhallar_instance* in, const double* p_host
   const int64_t np = in->h.np;
   std::vector<double> up(np), lo(np);
   for (int64_t k = 0; k < np; ++k) up[k] = p_host ? p_host[k] : 0.0;
-  for (int64_t e = 0; e < np; ++e) lo[e] = up[in->lo_eid_host[e]];
+  if (in->h.family != kPhaseret)
+    for (int64_t e = 0; e < np; ++e) lo[e] = up[in->lo_eid_host[e]];
   ck(cudaMemcpy(in->p_up, up.data(), np * sizeof(double), cudaMemcpyHostToDevice), "p_up");
   ck(cudaMemcpy(in->p_lo, lo.data(), np * sizeof(double), cudaMemcpyHostToDevice), "p_lo");
   in->h2d += int64_t(2 * np * sizeof(double));
   return (in->h.has_trace && p_host) ? p_host[np] : 0.0;
+}
+
+static int fill_report(cuhallar_instance* in, const SolveOut& so, float ms, double wall,
+                       cuhallar_report* rep, cuhallar_solution** sol,
+                       const std::vector<cuhallar_instance*>& ranks);
+
+// Start point into buffer 0: warm-start factor, or u0 = gaussian_vector(n,
+// Rng(seed)) / |u0| (solver.cpp:126-134).  Returns its rank.
+static int upload_start(cuhallar_instance* in, const cuhallar_config* cfg, const double* U0_host,
+                        int s0) {
+  const int64_t n = in->h.n;
+  if (U0_host) {
+    if (s0 < 1 || s0 > kSMax) throw hh::InputError("solve: warm-start rank must be in [1, 32]");
+    std::vector<double> tmp(U0_host, U0_host + n * s0);
+    const double nrm = std::sqrt(hh::eigen_order_sum_sq(tmp.data(), n * s0));
+    if (!(nrm <= 1.0 + 1e-12)) throw hh::InputError("solve: warm-start factor outside unit ball");
+    host_factor_to_buf0(in, U0_host, s0);
+    return s0;
+  }
+  std::vector<double> u0 = hh::gaussian_stream(cfg->seed, n);
+  const double nu = std::sqrt(hh::eigen_order_sum_sq(u0.data(), n));
+  for (auto& x : u0) x = x / nu;
+  ck(cudaMemcpy(in->buf[0], u0.data(), n * sizeof(double), cudaMemcpyHostToDevice), "U0");
+  in->h2d += int64_t(n * sizeof(double));
+  return 1;
 }
 
 int cuhallar_solve(cuhallar_instance* in, const cuhallar_config* cfg, const double* U0_host,
@@ -792,29 +949,14 @@ int cuhallar_solve(cuhallar_instance* in, const cuhallar_config* cfg, const doub
                    cuhallar_trace_fn fn, void* user) {
   return guard([&] {
     check_pairs(in);
+    DevGuard dg(in->device);
     validate_cfg(*cfg);
     std::lock_guard<std::mutex> lk(in->mu);
     const auto t_start = std::chrono::steady_clock::now();
     const int64_t n = in->h.n;
     const int grid = grid_size(cfg->team_ctas);
     ensure_workspace(in, grid, cfg->seed, cfg->eig_block_restart);
-    int s = 1;
-    if (U0_host) {
-      if (s0 < 1 || s0 > kSMax) throw hh::InputError("solve: warm-start rank must be in [1, 32]");
-      double nrm = 0.0;
-      std::vector<double> tmp(U0_host, U0_host + n * s0);
-      nrm = std::sqrt(hh::eigen_order_sum_sq(tmp.data(), n * s0));
-      if (!(nrm <= 1.0 + 1e-12)) throw hh::InputError("solve: warm-start factor outside unit ball");
-      s = s0;
-      host_factor_to_buf0(in, U0_host, s);
-    } else {
-      // u0 = gaussian_vector(n, Rng(seed)); U0 = u0/|u0|  (solver.cpp:130-132)
-      std::vector<double> u0 = hh::gaussian_stream(cfg->seed, n);
-      const double nu = std::sqrt(hh::eigen_order_sum_sq(u0.data(), n));
-      for (auto& x : u0) x = x / nu;
-      ck(cudaMemcpy(in->buf[0], u0.data(), n * sizeof(double), cudaMemcpyHostToDevice), "U0");
-      in->h2d += int64_t(n * sizeof(double));
-    }
+    const int s = upload_start(in, cfg, U0_host, s0);
     Params P = base_params(in, cfg);
     P.op = kOpSolve;
     P.s_in = s;
@@ -845,6 +987,20 @@ int cuhallar_solve(cuhallar_instance* in, const cuhallar_config* cfg, const doub
         fn(&ev, user);
       }
     }
+    (void)n;
+    return fill_report(in, so, ms, wall, rep, sol, {in});
+  });
+}
+
+// The SolveOut of a finished solve -> SolveReport (tau rescaling as finish(),
+// solver.cpp:175-202) and, on request, the solution.  For a sharded solve,
+// ranks[r] holds the multiplier entries of its rows; U is complete on rank 0.
+static int fill_report(cuhallar_instance* in, const SolveOut& so, float ms, double wall,
+                       cuhallar_report* rep, cuhallar_solution** sol,
+                       const std::vector<cuhallar_instance*>& ranks) {
+  {
+    const int stt = so.status;
+    const int64_t n = in->h.n;
     if (stt != 0 && stt != 1 && stt != 2 && stt != 3) return status_to_rc(stt, so.msg);
     if (so.status == kErrInput || so.status == kErrCapacity) return status_to_rc(so.status, so.msg);
     const double tau = in->h.tau;
@@ -881,12 +1037,158 @@ int cuhallar_solve(cuhallar_instance* in, const cuhallar_config* cfg, const doub
       for (int64_t a = 0; a < n; ++a)
         for (int k = 0; k < so.rank; ++k) S->U[a + k * n] = rm[a * so.rank + k];
       S->p.resize(in->h.m);
-      ck(cudaMemcpy(S->p.data(), in->p_up, in->h.np * sizeof(double), cudaMemcpyDeviceToHost),
-         "p out");
+      const int world = int(ranks.size());
+      if (world == 1) {
+        ck(cudaMemcpy(S->p.data(), in->p_up, in->h.np * sizeof(double), cudaMemcpyDeviceToHost),
+           "p out");
+      } else {
+        const int64_t nt = int64_t(in->tile_row_host.size()) - 1;
+        for (int r = 0; r < world; ++r) {
+          const int64_t rl = in->tile_row_host[nt * r / world];
+          const int64_t rh = in->tile_row_host[nt * (r + 1) / world];
+          const int64_t k0 = in->up_ptr_host[rl], k1 = in->up_ptr_host[rh];
+          DevGuard dg(ranks[r]->device);
+          if (k1 > k0)
+            ck(cudaMemcpy(S->p.data() + k0, ranks[r]->p_up + k0, (k1 - k0) * sizeof(double),
+                          cudaMemcpyDeviceToHost),
+               "p out");
+        }
+      }
       if (in->h.has_trace) S->p[in->h.np] = so.p_trace;
       *sol = S.release();
     }
     return 0;
+  }
+}
+
+int cuhallar_solve_sharded(cuhallar_instance* const* insts, int world, const cuhallar_config* cfg,
+                           const double* U0_host, int s0, const double* p0_host,
+                           cuhallar_report* rep, cuhallar_solution** sol) {
+  return guard([&] {
+    if (world < 1 || world > kMaxWorld) throw hh::InputError("sharded solve: world must lie in [1, 8]");
+    validate_cfg(*cfg);
+    std::vector<cuhallar_instance*> R(insts, insts + world);
+    for (int r = 0; r < world; ++r) {
+      if (!R[r]) throw hh::InputError("sharded solve: null instance");
+      if (R[r]->h.family == kPhaseret)
+        throw hh::InputError("sharded solve: phase retrieval does not shard (replicas only)");
+      if (R[r]->h.n != R[0]->h.n || R[r]->h.m != R[0]->h.m || R[r]->h.np != R[0]->h.np ||
+          R[r]->tile_row_host != R[0]->tile_row_host)
+        throw hh::InputError("sharded solve: ranks hold different instances");
+      for (int q = 0; q < r; ++q)
+        if (R[q] == R[r]) throw hh::InputError("sharded solve: one instance per rank");
+    }
+    std::vector<std::unique_lock<std::mutex>> locks;
+    for (auto* in : R) locks.emplace_back(in->mu);
+    int prev = 0;
+    ck(cudaGetDevice(&prev), "device");
+    struct Restore {
+      int d;
+      ~Restore() { cudaSetDevice(d); }
+    } restore{prev};
+    const auto t_start = std::chrono::steady_clock::now();
+    // peer access between distinct devices (NVLink / NVSwitch)
+    std::vector<int> share(world, 0);
+    for (int r = 0; r < world; ++r)
+      for (int q = 0; q < world; ++q) {
+        if (R[q]->device == R[r]->device) {
+          ++share[r];
+          continue;
+        }
+        int ok = 0;
+        ck(cudaDeviceCanAccessPeer(&ok, R[r]->device, R[q]->device), "peer query");
+        if (!ok) throw CudaError("sharded solve: devices without peer access");
+        ck(cudaSetDevice(R[r]->device), "device");
+        const cudaError_t e = cudaDeviceEnablePeerAccess(R[q]->device, 0);
+        if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+        else ck(e, "peer enable");
+      }
+    // equal team per rank; ranks sharing a device split its SMs (co-resident launches)
+    int G = kMaxTeam;
+    for (int r = 0; r < world; ++r) {
+      ck(cudaSetDevice(R[r]->device), "device");
+      G = std::min(G, grid_size(0) / share[r]);
+    }
+    if (cfg->team_ctas > 0) G = std::min(G, cfg->team_ctas);
+    if (G < 1) throw CudaError("sharded solve: not enough SMs for the ranks");
+    int s = 1;
+    for (int r = 0; r < world; ++r) {  // every rank's state exists before any Params is built
+      cuhallar_instance* in = R[r];
+      ck(cudaSetDevice(in->device), "device");
+      ensure_workspace(in, G, cfg->seed, cfg->eig_block_restart);
+      if (!in->xbar) {
+        in->xbar = dalloc<unsigned long long>(1, &in->bytes);
+        in->xslots = dalloc<double>(size_t(2) * kMaxWorld * kRedK, &in->bytes);
+        in->xerr = dalloc<int>(1, &in->bytes);
+      }
+      ck(cudaMemset(in->xbar, 0, sizeof(unsigned long long)), "xbar");
+      ck(cudaMemset(in->xerr, 0, sizeof(int)), "xerr");
+    }
+    std::vector<Params> Ps(world);
+    for (int r = 0; r < world; ++r) {
+      cuhallar_instance* in = R[r];
+      ck(cudaSetDevice(in->device), "device");
+      s = upload_start(in, cfg, U0_host, s0);
+      Params& P = Ps[r];
+      P = base_params(in, cfg);
+      P.op = kOpSolve;
+      P.s_in = s;
+      P.p_trace = host_multiplier_to_dev(in, p0_host);
+      P.fab.world = world;
+      P.fab.me = r;
+      P.fab.arena_len = in->arena_len;
+      P.fab.xerr = in->xerr;
+      for (int q = 0; q < world; ++q) {
+        P.fab.xbar[q] = R[q]->xbar;
+        P.fab.xslots[q] = R[q]->xslots;
+        P.fab.arena[q] = R[q]->arena;
+      }
+    }
+    // all ranks in flight before any wait: the team needs every launch resident
+    std::vector<cudaStream_t> st(world);
+    std::vector<cudaEvent_t> e0(world), e1(world);
+    for (int r = 0; r < world; ++r) {
+      cuhallar_instance* in = R[r];
+      ck(cudaSetDevice(in->device), "device");
+      ck(cudaStreamCreateWithFlags(&st[r], cudaStreamNonBlocking), "stream");
+      ck(cudaEventCreate(&e0[r]), "event");
+      ck(cudaEventCreate(&e1[r]), "event");
+      ck(cudaMemsetAsync(in->bar, 0, sizeof(unsigned long long), st[r]), "bar");
+      ck(cudaMemsetAsync(in->dso, 0, sizeof(SolveOut), st[r]), "dso");
+      if (in->trace_count_host) *in->trace_count_host = 0;
+      ck(cudaEventRecord(e0[r], st[r]), "event");
+      SolveOut* dso = in->dso;
+      void* args[] = {&Ps[r], &dso};
+      ck(cudaLaunchCooperativeKernel((void*)hallar_kernel, dim3(G), dim3(kThreads), args,
+                                     kSmemBytes, st[r]),
+         "cooperative launch (sharded)");
+      ck(cudaEventRecord(e1[r], st[r]), "event");
+    }
+    float ms = 0.f;
+    int xerr = 0;
+    for (int r = 0; r < world; ++r) {
+      ck(cudaSetDevice(R[r]->device), "device");
+      ck(cudaStreamSynchronize(st[r]), "hallar_kernel (sharded)");
+      float t = 0.f;
+      ck(cudaEventElapsedTime(&t, e0[r], e1[r]), "event");
+      ms = std::max(ms, t);  // device time of the solve = max over ranks
+      int e = 0;
+      ck(cudaMemcpy(&e, R[r]->xerr, sizeof(int), cudaMemcpyDeviceToHost), "xerr");
+      xerr |= e;
+      cudaEventDestroy(e0[r]);
+      cudaEventDestroy(e1[r]);
+      cudaStreamDestroy(st[r]);
+    }
+    ck(cudaSetDevice(R[0]->device), "device");
+    SolveOut so{};
+    ck(cudaMemcpy(&so, R[0]->dso, sizeof(SolveOut), cudaMemcpyDeviceToHost), "D2H out");
+    if (xerr && so.status == kOk) {
+      so.status = kErrFabric;
+      so.msg = kMsgFabric;
+    }
+    const double wall =
+        std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();
+    return fill_report(R[0], so, ms, wall, rep, sol, R);
   });
 }
 
@@ -916,6 +1218,7 @@ int cuhallar_min_eig_gradient(cuhallar_instance* in, const double* U_host, int s
                               double* residual, int* matvecs, int* converged) {
   return guard([&] {
     check_pairs(in);
+    DevGuard dg(in->device);
     if (s < 1 || s > kSMax) throw hh::InputError("factor rank must be in [1, 32]");
     if (block_restart < 2 || block_restart > kLanczosMax)
       throw hh::InputError("eig: block_restart must lie in [2, 32]");
@@ -958,6 +1261,7 @@ int cuhallar_aipp(cuhallar_instance* in, const double* p_host, double beta, cons
                   double* lambda) {
   return guard([&] {
     check_pairs(in);
+    DevGuard dg(in->device);
     if (s < 1 || s > kSMax) throw hh::InputError("factor rank must be in [1, 32]");
     std::lock_guard<std::mutex> lk(in->mu);
     const int grid = grid_size(cfg ? cfg->team_ctas : 0);
@@ -998,6 +1302,7 @@ int cuhallar_bench_pass(cuhallar_instance* in, int kind, const double* U_host, i
                         double* ns_per_pass) {
   return guard([&] {
     check_pairs(in);
+    DevGuard dg(in->device);
     if (s < 1 || s > kSMax) throw hh::InputError("factor rank must be in [1, 32]");
     std::lock_guard<std::mutex> lk(in->mu);
     const int grid = grid_size(team_ctas);

@@ -17,8 +17,25 @@ constexpr int kGroups = 4;               // independent 128-thread tile groups p
 constexpr int kGT = kThreads / kGroups;  // threads per tile group
 constexpr int kTileEntries = 512;        // entries per row tile (per group)
 constexpr int kTileRows = 32;            // rows per row tile
+constexpr int kPrMaxNc = 8192;           // phase retrieval: transform length held in smem
+// shared scratch of one pass: the tile engine's arrays or one complex transform
+constexpr int kTileDoubles = kGroups * (5 * kTileEntries + 4 * (kTileRows + 1) + kTileEntries / 2);
+constexpr int kPassScratch = kTileDoubles > 2 * kPrMaxNc ? kTileDoubles : 2 * kPrMaxNc;
 
 enum Family : int { kTheta = 0, kMatcomp = 1, kPhaseret = 2 };
+
+// Row-sharded solve across GPUs: one persistent launch per
+// rank; the ranks address each other's memory through peer pointers.
+constexpr int kMaxWorld = 8;
+struct Fabric {
+  int world = 1, me = 0;
+  unsigned long long* xbar[kMaxWorld] = {};  // rank-rendezvous counter on each rank
+  double* xslots[kMaxWorld] = {};            // [2][kMaxWorld][kRedK] per-rank partials on each rank
+  double* arena[kMaxWorld] = {};             // replicated factor arena on each rank
+  int64_t arena_len = 0;                     // doubles
+  int* xerr = nullptr;                       // this rank's error flag (rendezvous timeout)
+  unsigned long long timeout_ns = 20000000000ull;
+};
 
 // Optional in-solve phase profile (CTA 0's %globaltimer between phase ends).
 enum ProfCat : int {
@@ -31,6 +48,7 @@ enum Status : int {
   kErrInput = 64,
   kErrNumerical = 3,
   kErrCapacity = 65,  // rank or Lanczos refill capacity exceeded
+  kErrFabric = 71,    // sharded team: a peer rank did not arrive
 };
 
 // Pair-constraint instance as resident in HBM (theta / graph / matcomp).
@@ -58,6 +76,13 @@ struct DevPairs {
   const int64_t* tile_row = nullptr;  // [ntiles+1] first row of each row tile
   int64_t ntiles = 0;
   double norm_b1 = 0.0, nb2 = 0.0, norm_C1 = 0.0;  // scaled instance norms
+  // phase retrieval (family kPhaseret): np = m, b_up = b (constraint order)
+  int64_t nc = 0;                 // complex dimension (n = 2 nc)
+  int L = 0, lognc = 0;           // masks, log2(nc)
+  const double2* masks = nullptr; // nc x L column-major
+  const double2* twid = nullptr;  // FftPlan forward twiddles (nc - 1)
+  double2* F = nullptr;           // spectrum cache [kSMax][m]
+  double2* G = nullptr;           // adjoint partials [kSMax][L][nc]
 };
 
 // Solver configuration (mirrors cuhallar_config / SolverConfig).
@@ -103,6 +128,7 @@ struct Params {
   DevPairs I;
   Cfg cfg;
   // team
+  Fabric fab;
   unsigned long long* bar = nullptr;
   double* slots = nullptr;  // [2][G][kRedK]
   // factor pool, row-major n x s (stride s) inside capacity n x kSMax

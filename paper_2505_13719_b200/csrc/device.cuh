@@ -13,6 +13,7 @@
 
 #include "common.cuh"
 #include "team.cuh"
+#include "pr.cuh"
 
 namespace hallar {
 
@@ -32,6 +33,7 @@ enum Msg : int {
   kMsgRankCap = 8,
   kMsgRefillCap = 9,
   kMsgRank32 = 10,
+  kMsgFabric = 11,
 };
 
 struct Ctx {
@@ -42,6 +44,7 @@ struct Ctx {
   double* tw;     // [kTileEntries] w per entry
   int32_t* tcol;  // [kTileEntries] gathered row per entry
   double* tterm;  // [kTileEntries * 4] w * U(b, c), c < 4
+  double2* X;     // phase retrieval transform buffer (aliases the tile arrays)
   double* cs;     // [kSMax] column sums of the gathered factor (theta C-term)
   double* H;      // [kHLd][kHLd] Lanczos projected matrix (column-major)
   double* JA;     // [32*32] Jacobi work
@@ -130,11 +133,13 @@ __device__ int64_t row_split(const DevPairs& I, int rank, int size) {
 struct UPlain {
   const double* __restrict__ U;
   __device__ __forceinline__ double operator()(int64_t o) const { return U[o]; }
+  __device__ __forceinline__ const double* base() const { return U; }
 };
 struct UScaled {  // Lanczos: v = src / scale, materialised on the fly
   const double* __restrict__ src;
   double sc;
   __device__ __forceinline__ double operator()(int64_t o) const { return src[o] / sc; }
+  __device__ __forceinline__ const double* base() const { return src; }
 };
 
 __device__ __forceinline__ void group_sync(int g) {
@@ -161,6 +166,7 @@ __device__ __forceinline__ void row_pass_t(Ctx& c, const Params& P, const UA& U,
   double* const tterm = c.tterm + g * 4 * kTileEntries;
   const int nthr = (kGT / s) * s;  // phase-3 threads of the group; column = gt % s
   const int mycol = gt % s;
+  publish_rows(c.t, U.base(), c.rl, c.rh, s);  // sharded: gathered rows -> every rank
 
   auto vlo = [&](int buf) { return vlo0 + buf * (kTileRows + 1); };
   auto vup = [&](int buf) { return vup0 + buf * (kTileRows + 1); };
@@ -425,6 +431,7 @@ __device__ __forceinline__ void gradop_pass(Ctx& c, const Params& P, const doubl
   const int s = S > 0 ? S : s_rt;
   const int lane = c.lane;
   bool bad = false;
+  publish_rows(c.t, U, c.rl, c.rh, s);
   for (int64_t a = c.rl + c.warp; a < c.rh; a += kWarps) {
     double ua[SR];
 #pragma unroll
@@ -499,6 +506,7 @@ __device__ __forceinline__ void map_pass_src(Ctx& c, const Params& P, const RowS
                                           const double* __restrict__ ref, double (&sums)[2]) {
   const DevPairs& I = P.I;
   const int s = S > 0 ? S : s_rt;
+  if (src.U) publish_rows(c.t, src.U, c.rl, c.rh, s);
   for (int64_t k0 = c.kl + threadIdx.x; k0 < c.kh; k0 += (int64_t)kThreads * kUnroll) {
     int64_t ii[kUnroll], jj[kUnroll];
     double pk[kUnroll], bk[kUnroll], rf[kUnroll];
@@ -625,9 +633,10 @@ __device__ __forceinline__ void factor_stats(Ctx& c, const Params& P, const doub
   factor_stats_to<S>(c, P, U, s_rt, nrm2, c.cs);
 }
 
-// <CU, U> from the statistics: theta -sum_c cs_c^2, MC 0.5||U||^2.
+// <CU, U> from the statistics: theta -sum_c cs_c^2, MC 0.5||U||^2, PR ||U||^2.
 __device__ __forceinline__ double cdot_from_stats(const double* cs, const DevPairs& I, int s,
                                                   double nrm2) {
+  if (is_pr(I)) return nrm2;  // C = I (instances.cpp:350)
   if (is_theta(I)) {
     double t = 0.0;
     for (int k = 0; k < s; ++k) t = t + cs[k] * cs[k];
@@ -660,7 +669,17 @@ __device__ __noinline__ bool al_value_dev(Ctx& c, const Params& P, const double*
   double nrm2;
   factor_stats<S>(c, P, U, s, &nrm2);
   double sums[2] = {0.0, 0.0};
-  map_pass<S>(c, P, U, s, kMapPR, pup, nullptr, nullptr, sums);
+  if (is_pr(I)) {
+    pr_forward(P, c.t.rank, c.t.size, c.X, UPlain{U}, s);
+    c.t.sync();
+    pr_map_combine(P, c.kl, c.kh, s, [&](int64_t k, double d) {
+      const double r = d - I.b_up[k];
+      sums[0] = sums[0] + pup[k] * r;
+      sums[1] = sums[1] + r * r;
+    });
+  } else {
+    map_pass<S>(c, P, U, s, kMapPR, pup, nullptr, nullptr, sums);
+  }
   team_sum<2>(c.t, c.rs, sums);
   double pr = sums[0], rr = sums[1];
   if (is_theta(I)) {
@@ -714,7 +733,7 @@ __device__ __noinline__ bool fista_dev(Ctx& c, const Params& P, Roles& R, int s,
   const bool theta = is_theta(I);
   // y+ recomputed inside the map (saves a barrier) while the instance is
   // latency-bound; beyond ~2^20 factor entries the divisions would dominate
-  const bool fuse_y = I.n * (int64_t)s <= (int64_t(1) << 20);
+  const bool fuse_y = !is_pr(I) && !c.t.multi() && I.n * (int64_t)s <= (int64_t(1) << 20);
   double A = 0.0, tau = 1.0, L = L0;
   double* csx = c.cs + kSMax;  // column sums of x~ (kept apart from c.cs)
   prof_mark(c, P, kPfAipp);
@@ -732,6 +751,10 @@ __device__ __noinline__ bool fista_dev(Ctx& c, const Params& P, Roles& R, int s,
   bool pre = false;  // x~ and its statistics already produced by T5
   double dd = 0.0, nt2 = 0.0;
   for (int it = 0;; ++it) {
+    if (c.t.xfailed) {
+      fail(c, kErrFabric, kMsgFabric);
+      return false;
+    }
     const int cap = cf.fista_max_iters > 0
                         ? cf.fista_max_iters
                         : 50 + (int)(10.0 * sqrt(L / mu) * log2(4.0 + L / L0));
@@ -789,8 +812,16 @@ __device__ __noinline__ bool fista_dev(Ctx& c, const Params& P, Roles& R, int s,
           zz = zz + z * z;
         };
         double sums[3] = {0.0, 0.0, 0.0};
-        row_pass<S, false>(c, P, XT, s, P.p_up, P.p_lo, beta, theta_alpha_or_half(I, qt),
-                           theta ? csx : nullptr, false, sums, epi);
+        if (is_pr(I)) {
+          pr_forward(P, c.t.rank, c.t.size, c.X, UPlain{XT}, s);
+          c.t.sync();
+          pr_inverse<false>(P, c.t.rank, c.t.size, c.X, s, nullptr, P.p_up, beta, sums);
+          c.t.sync();
+          pr_combine(P, c.rl, c.rh, UPlain{XT}, s, true, epi);
+        } else {
+          row_pass<S, false>(c, P, XT, s, P.p_up, P.p_lo, beta, theta_alpha_or_half(I, qt),
+                             theta ? csx : nullptr, false, sums, epi);
+        }
         double v[5] = {hU, sums[0], sums[1], sums[2], zz};
         team_sum<5>(c.t, c.rs, v);
         prof_mark(c, P, kPfT2);
@@ -846,7 +877,17 @@ __device__ __noinline__ bool fista_dev(Ctx& c, const Params& P, Roles& R, int s,
           src.U = YN;
         }
         double ms[2] = {0.0, 0.0};
-        map_pass_src<S>(c, P, src, s, kMapPR, P.p_up, nullptr, nullptr, ms);
+        if (is_pr(I)) {
+          pr_forward(P, c.t.rank, c.t.size, c.X, UPlain{YN}, s);
+          c.t.sync();
+          pr_map_combine(P, c.kl, c.kh, s, [&](int64_t k, double d) {
+            const double r = d - I.b_up[k];
+            ms[0] = ms[0] + P.p_up[k] * r;
+            ms[1] = ms[1] + r * r;
+          });
+        } else {
+          map_pass_src<S>(c, P, src, s, kMapPR, P.p_up, nullptr, nullptr, ms);
+        }
         double v[6] = {v3[0], v3[1], v3[2], v3[3], ms[0], ms[1]};
         stage_scalars<6>(c, v);
         team_reduce_smem(c.t, c.rs, 6 + s);
@@ -925,8 +966,15 @@ __device__ __noinline__ bool fista_dev(Ctx& c, const Params& P, Roles& R, int s,
         }
       };
       double sums[3] = {0.0, 0.0, 0.0};
-      row_pass<S, false>(c, P, YN, s, P.p_up, P.p_lo, beta, theta_alpha_or_half(I, qt),
-                         theta ? c.cs : nullptr, false, sums, epi);
+      if (is_pr(I)) {
+        // spectra of y+ are still cached from T34
+        pr_inverse<false>(P, c.t.rank, c.t.size, c.X, s, nullptr, P.p_up, beta, sums);
+        c.t.sync();
+        pr_combine(P, c.rl, c.rh, UPlain{YN}, s, true, epi);
+      } else {
+        row_pass<S, false>(c, P, YN, s, P.p_up, P.p_lo, beta, theta_alpha_or_half(I, qt),
+                           theta ? c.cs : nullptr, false, sums, epi);
+      }
       double v[3] = {vv, ddn, ntn};
       stage_scalars<3>(c, v);
       stage_colsums(c, s, 3, csn);

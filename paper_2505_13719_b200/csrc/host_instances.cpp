@@ -422,8 +422,11 @@ HostInst make_phaseret(int64_t n, int L, uint64_t seed, double tau_slack) {
       const double ang = -2.0 * M_PI * double(k) / double(len);
       h.twiddle.emplace_back(std::cos(ang), std::sin(ang));
     }
-  double sx = 0.0;  // ||x||^2 (sequential complex abs2 sum)
-  for (auto& z : h.hidden_x) sx += z.real() * z.real() + z.imag() * z.imag();
+  // ||x||^2 in the oracle's reduction order (hidden_x.squaredNorm())
+  const double sx = eigen_sum(n, [&](int64_t j) {
+    const auto& z = h.hidden_x[j];
+    return z.real() * z.real() + z.imag() * z.imag();
+  });
   h.tau = tau_slack * sx;
   h.norm_C1 = double(2 * n);
   // b is computed on the device (map of the hidden signal) by the caller.

@@ -1,0 +1,214 @@
+// Phase retrieval (coded diffraction patterns) operator inside the persistent
+// kernel — instances.cpp:236-389 (PrData::map_column / adjoint_column) over
+// FftPlan (fft.cpp:57-100).
+//
+// Real embedding: factor rows a < nc are Re u_j, rows nc + j are Im u_j
+// (load_column, instances.cpp:266-269).  Constraint k = l*nc + kk is
+// |FFT(d_l .* u)_kk|^2 summed over factor columns.
+//
+// Work split (a "task" is one (column c, mask l) transform, one CTA each,
+// round-robin over the team; the whole length-nc transform lives in shared
+// memory, nc <= kPrMaxNc):
+//   forward  F[c][k] = FFT(d_l .* u_c)      -> HBM (spectrum cache, c*m + k)
+//   inverse  G[c][l] = conj(d_l) .* IFFT(q_l .* F[c][l])  -> HBM
+//   combine  row a, column c: sum_l G[c][l][j] (l increasing), +U for C = I
+// The spectrum of the factor is computed once per factor and reused by the
+// adjoint (the reference recomputes it in adjoint_column: same operands, so
+// the cached values are bit-identical).
+//
+// Arithmetic matches the reference under -fcx-limited-range:
+// complex products (ac - bd, ad + bc), std::norm = re^2 + im^2, real scaling
+// per component, and the same radix-2 butterfly DAG and twiddle table — the
+// register-blocked passes below apply 2^R stages of the radix-2 network per
+// shared-memory round trip, each butterfly with the reference's operands, so
+// every output is bit-identical to the reference transform.
+#pragma once
+
+#include "common.cuh"
+
+namespace hallar {
+
+__device__ __forceinline__ bool is_pr(const DevPairs& I) { return I.family == kPhaseret; }
+
+__device__ __forceinline__ double2 cmul(const double2 a, const double2 b) {
+  return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+
+// bit-reversal permutation of FftPlan (fft.cpp:60-66)
+__device__ __forceinline__ int brev_idx(int j, int logn) {
+  return (int)(__brev((unsigned)j) >> (32 - logn));
+}
+
+// R consecutive radix-2 stages (halves h, 2h, ..., 2^(R-1) h, h = 2^st) with
+// the 2^R operands of each butterfly group held in registers.
+template <int R, bool INV>
+__device__ __forceinline__ void fft_pass(double2* X, int nc, int st,
+                                         const double2* __restrict__ tw) {
+  constexpr int E = 1 << R;
+  const int h = 1 << st;
+  const int groups = nc >> R;
+  for (int gi = threadIdx.x; gi < groups; gi += kThreads) {
+    const int k = gi & (h - 1);
+    const int base = ((gi >> st) << (st + R)) + k;
+    double2 v[E];
+#pragma unroll
+    for (int t = 0; t < E; ++t) v[t] = X[base + t * h];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int hr = h << r;
+#pragma unroll
+      for (int t = 0; t < E; ++t) {
+        if (t & (1 << r)) continue;
+        // position of the butterfly inside its length-2hr block
+        const int kk = k + (t & ((1 << r) - 1)) * h;
+        double2 w = __ldg(tw + (hr - 1) + kk);  // stage table offset = hr - 1
+        if (INV) w.y = -w.y;                    // std::conj(tw[k]) (fft.cpp:87)
+        const double2 u = v[t];
+        const double2 x = cmul(v[t + (1 << r)], w);
+        v[t] = make_double2(u.x + x.x, u.y + x.y);
+        v[t + (1 << r)] = make_double2(u.x - x.x, u.y - x.y);
+      }
+    }
+#pragma unroll
+    for (int t = 0; t < E; ++t) X[base + t * h] = v[t];
+  }
+  __syncthreads();
+}
+
+// In-place transform of the bit-reversed X (FftPlan::run after the swaps).
+template <bool INV>
+__device__ __forceinline__ void fft_smem(double2* X, int nc, int logn,
+                                         const double2* __restrict__ tw) {
+  int st = 0;
+  for (; logn - st >= 3; st += 3) fft_pass<3, INV>(X, nc, st, tw);
+  if (logn - st == 2) fft_pass<2, INV>(X, nc, st, tw);
+  else if (logn - st == 1) fft_pass<1, INV>(X, nc, st, tw);
+}
+
+// Forward tasks: F[c*m + l*nc + k] = FFT(d_l .* u_c)_k for c < s, l < L.
+// U(o) returns factor element o = row * s + column.  Caller team-syncs
+// before (U complete) and after (F complete).
+template <class UA>
+__device__ __noinline__ void pr_forward(const Params& P, int rank, int size, double2* X, const UA U,
+                                        int s) {
+  const DevPairs& I = P.I;
+  const int nc = (int)I.nc, L = I.L, logn = I.lognc;
+  for (int task = rank; task < s * L; task += size) {
+    const int col = task / L, l = task % L;
+    const double2* mk = I.masks + (int64_t)l * nc;
+    for (int p = threadIdx.x; p < nc; p += kThreads) {
+      const int j = brev_idx(p, logn);
+      const double2 u = make_double2(U((int64_t)j * s + col), U((int64_t)(nc + j) * s + col));
+      X[p] = cmul(__ldg(mk + j), u);  // masks(j,l) * u(j)  (instances.cpp:273)
+    }
+    __syncthreads();
+    fft_smem<false>(X, nc, logn, I.twid);
+    double2* F = I.F + (int64_t)col * I.m + (int64_t)l * nc;
+    for (int k = threadIdx.x; k < nc; k += kThreads) F[k] = X[k];
+    __syncthreads();
+  }
+}
+
+// d_k = sum_c |F[c][k]|^2 in column order: partial.rowwise().sum() over the
+// per-column slabs, each slab 0 + norm (instances.cpp:276, 353-361).
+__device__ __forceinline__ double pr_map_value(const DevPairs& I, int64_t k, int s) {
+  double d = 0.0;
+  for (int cc = 0; cc < s; ++cc) {
+    const double2 g = I.F[(int64_t)cc * I.m + k];
+    const double t = g.x * g.x + g.y * g.y;
+    d = (cc == 0) ? t : d + t;
+  }
+  return d;
+}
+
+// Inverse tasks: G[(c*L + l)*nc + j] = conj(d_l) .* IFFT_unscaled(q_l .* F[c][l])
+// (adjoint_column, instances.cpp:281-293).  FIXED: q given (m-vector);
+// otherwise q = p + beta (d - b) from the cached spectra, and the tasks of
+// column 0 accumulate sums[0] += p r, sums[1] += r^2, sums[2] += q (r + b)
+// over every constraint once.
+template <bool FIXED>
+__device__ __noinline__ void pr_inverse(const Params& P, int rank, int size, double2* X, int s,
+                                        const double* __restrict__ qv,
+                                        const double* __restrict__ pv, double beta,
+                                        double* sums) {
+  const DevPairs& I = P.I;
+  const int nc = (int)I.nc, L = I.L, logn = I.lognc;
+  const double* __restrict__ bv = I.b_up;
+  for (int task = rank; task < s * L; task += size) {
+    const int col = task / L, l = task % L;
+    const int64_t off = (int64_t)l * nc;
+    const double2* Fc = I.F + (int64_t)col * I.m + off;
+    for (int p = threadIdx.x; p < nc; p += kThreads) {
+      const int k = brev_idx(p, logn);
+      const double2 f = Fc[k];
+      double q;
+      if (FIXED) {
+        q = qv[off + k];
+      } else {
+        const double d = pr_map_value(I, off + k, s);
+        const double bb = bv ? bv[off + k] : 0.0;
+        const double r = d - bb;
+        const double pk = pv[off + k];
+        q = pk + beta * r;
+        if (col == 0) {
+          sums[0] = sums[0] + pk * r;
+          sums[1] = sums[1] + r * r;
+          sums[2] = sums[2] + q * (r + bb);
+        }
+      }
+      X[p] = make_double2(f.x * q, f.y * q);  // s.buf[k] *= pl[k]
+    }
+    __syncthreads();
+    fft_smem<true>(X, nc, logn, I.twid);
+    const double2* mk = I.masks + off;
+    double2* G = I.G + ((int64_t)col * L + l) * nc;
+    for (int j = threadIdx.x; j < nc; j += kThreads) {
+      const double2 m = __ldg(mk + j);
+      G[j] = cmul(make_double2(m.x, -m.y), X[j]);  // conj(masks(j,l)) * buf[j]
+    }
+    __syncthreads();
+  }
+}
+
+// Combine: for the CTA's rows a in [rl, rh) and columns c < s,
+//   h(a,c) = sum_l G[c][l][j] (component of row a) [+ U(a,c) when addC]
+// and epi(a, c, h, U(a,c)).  Thread -> column mapping is the tile engine's
+// (thread gt of a 128-thread group owns column gt % s), so per-column
+// epilogue accumulators and stage_colsums work unchanged.
+template <class UA, class Epi>
+__device__ __forceinline__ void pr_combine(const Params& P, int64_t rl, int64_t rh, const UA& U,
+                                           int s, bool addC, Epi& epi) {
+  const DevPairs& I = P.I;
+  const int64_t nc = I.nc;
+  const int L = I.L;
+  const int g = threadIdx.x / kGT, gt = threadIdx.x % kGT;
+  const int nthr = (kGT / s) * s;
+  const int64_t nrows = rh - rl;
+  const int64_t r0 = rl + nrows * g / kGroups, r1 = rl + nrows * (g + 1) / kGroups;
+  const int64_t cnt = gt < nthr ? (r1 - r0) * s : 0;
+  for (int64_t idx = gt; idx < cnt; idx += nthr) {
+    const int64_t a = r0 + idx / s;
+    const int col = (int)(idx % s);
+    const bool im = a >= nc;
+    const int64_t j = im ? a - nc : a;
+    const double* G = reinterpret_cast<const double*>(I.G + (int64_t)col * L * nc + j) + (im ? 1 : 0);
+    double acc = 0.0;
+    for (int l = 0; l < L; ++l) {
+      const double t = G[(int64_t)l * nc * 2];
+      acc = (l == 0) ? t : acc + t;
+    }
+    const double uo = U(a * s + col);
+    const double h = addC ? acc + uo : acc;  // out_m += U (instances.cpp:377)
+    epi(a, col, h, uo);
+  }
+  __syncthreads();  // rows written by the epilogue are read by other threads of the CTA next
+}
+
+// Map combine over the CTA's constraint range [kl, kh): f(k, d_k).
+template <class Fn>
+__device__ __forceinline__ void pr_map_combine(const Params& P, int64_t kl, int64_t kh, int s,
+                                               Fn&& f) {
+  for (int64_t k = kl + threadIdx.x; k < kh; k += kThreads) f(k, pr_map_value(P.I, k, s));
+}
+
+}  // namespace hallar

@@ -21,7 +21,16 @@ __device__ __noinline__ bool check_termination_dev(Ctx& c, const Params& P, cons
   double nrm2;
   factor_stats<S>(c, P, U, s, &nrm2);
   double ms[2] = {0.0, 0.0};
-  map_pass<S>(c, P, U, s, kMapRR, nullptr, nullptr, nullptr, ms);
+  if (is_pr(I)) {
+    pr_forward(P, c.t.rank, c.t.size, c.X, UPlain{U}, s);
+    c.t.sync();
+    pr_map_combine(P, c.kl, c.kh, s, [&](int64_t k, double d) {
+      const double r = d - I.b_up[k];
+      ms[1] = ms[1] + r * r;
+    });
+  } else {
+    map_pass<S>(c, P, U, s, kMapRR, nullptr, nullptr, nullptr, ms);
+  }
   double bp = 0.0;
   if (I.b_up)
     for (int64_t k = c.kl + threadIdx.x; k < c.kh; k += kThreads) bp = bp + I.b_up[k] * P.p_up[k];
@@ -115,6 +124,10 @@ __device__ __noinline__ void solve_dev(Ctx& c, const Params& P, SolveOut* so) {
   bool nan_report = false;
 
   for (int t = 1; t <= cf.max_outer; ++t) {
+    if (c.t.xfailed) {
+      fail(c, kErrFabric, kMsgFabric);
+      break;
+    }
     if (team_now(c) >= deadline) {
       status = 2;
       break;
@@ -164,10 +177,12 @@ __device__ __noinline__ void solve_dev(Ctx& c, const Params& P, SolveOut* so) {
         if (!isfinite(pn)) bad = 1.0;
         if (I.b_up) bp = bp + I.b_up[k] * pn;
       }
-      const int64_t lo_n = I.lo_ptr[c.rh] - I.lo_ptr[c.rl];
-      const int64_t lo0 = I.lo_ptr[c.rl];
-      for (int64_t e = threadIdx.x; e < lo_n; e += kThreads)
-        P.p_lo[lo0 + e] = P.p_lo[lo0 + e] + beta * P.r_lo[lo0 + e];
+      if (!is_pr(I)) {
+        const int64_t lo_n = I.lo_ptr[c.rh] - I.lo_ptr[c.rl];
+        const int64_t lo0 = I.lo_ptr[c.rl];
+        for (int64_t e = threadIdx.x; e < lo_n; e += kThreads)
+          P.p_lo[lo0 + e] = P.p_lo[lo0 + e] + beta * P.r_lo[lo0 + e];
+      }
       const double* U = P.buf[R.rep];
       for (int64_t a = c.rl + threadIdx.x; a < c.rh; a += kThreads)
         for (int k = 0; k < s; ++k)
@@ -251,6 +266,7 @@ __device__ __noinline__ void solve_dev(Ctx& c, const Params& P, SolveOut* so) {
     fc = ct;
     have_cert = true;
   }
+  publish_rows(c.t, P.buf[R.rep], c.rl, c.rh, s);  // sharded: rank 0 holds every row of U
   o.out_buf = R.rep;
   o.rank = s;
   o.msg = c.msg;
@@ -288,6 +304,12 @@ __device__ __noinline__ void op_dispatch(Ctx& c, const Params& P, SolveOut* so) 
       double nrm2;
       factor_stats<S>(c, P, U, s, &nrm2);
       double ms[2];
+      if (is_pr(I)) {
+        pr_forward(P, c.t.rank, c.t.size, c.X, UPlain{U}, s);
+        c.t.sync();
+        pr_map_combine(P, c.kl, c.kh, s, [&](int64_t k, double d) { P.out_vec[k] = d; });
+        break;
+      }
       map_pass<S>(c, P, U, s, kMapOut, nullptr, P.out_vec, nullptr, ms);
       if (is_theta(I) && c.t.rank == 0 && threadIdx.x == 0) P.out_vec[I.np] = nrm2;
       break;
@@ -300,6 +322,14 @@ __device__ __noinline__ void op_dispatch(Ctx& c, const Params& P, SolveOut* so) 
       double* out = P.out_mat;
       auto epi = [&](int64_t a, int cc, double h, double) { out[a * s + cc] = h; };
       double sums[3] = {0, 0, 0};
+      if (is_pr(I)) {
+        pr_forward(P, c.t.rank, c.t.size, c.X, UPlain{U}, s);
+        c.t.sync();
+        pr_inverse<true>(P, c.t.rank, c.t.size, c.X, s, P.q_up, nullptr, 0.0, sums);
+        c.t.sync();
+        pr_combine(P, c.rl, c.rh, UPlain{U}, s, withC, epi);
+        break;
+      }
       const double alpha = is_theta(I) ? P.q_trace_in : 0.5;
       const bool zero = !is_theta(I) && !withC;
       row_pass<S, true>(c, P, U, s, P.q_up, P.q_lo, 0.0, alpha,
@@ -311,7 +341,8 @@ __device__ __noinline__ void op_dispatch(Ctx& c, const Params& P, SolveOut* so) 
       factor_stats<S>(c, P, U, s, &nrm2);
       for (int64_t a = c.rl + threadIdx.x; a < c.rh; a += kThreads)
         for (int k = 0; k < s; ++k)
-          P.out_mat[a * s + k] = is_theta(I) ? -1.0 * c.cs[k] : 0.5 * U[a * s + k];
+          P.out_mat[a * s + k] = is_pr(I) ? U[a * s + k]
+                                 : is_theta(I) ? -1.0 * c.cs[k] : 0.5 * U[a * s + k];
       break;
     }
     case kOpAlValue: {
@@ -340,8 +371,16 @@ __device__ __noinline__ void op_dispatch(Ctx& c, const Params& P, SolveOut* so) 
         out[a * s + cc] = g;
       };
       double sums[3] = {0, 0, 0};
-      row_pass<S, false>(c, P, U, s, P.p_up, P.p_lo, beta, theta_alpha_or_half(I, qt),
-                         is_theta(I) ? c.cs : nullptr, false, sums, epi);
+      if (is_pr(I)) {
+        pr_forward(P, c.t.rank, c.t.size, c.X, UPlain{U}, s);
+        c.t.sync();
+        pr_inverse<false>(P, c.t.rank, c.t.size, c.X, s, nullptr, P.p_up, beta, sums);
+        c.t.sync();
+        pr_combine(P, c.rl, c.rh, UPlain{U}, s, true, epi);
+      } else {
+        row_pass<S, false>(c, P, U, s, P.p_up, P.p_lo, beta, theta_alpha_or_half(I, qt),
+                           is_theta(I) ? c.cs : nullptr, false, sums, epi);
+      }
       double v[5] = {hU, sums[0], sums[1], sums[2], bad};
       team_sum<5>(c.t, c.rs, v);
       double pr = v[1], rr = v[2], qrb = v[3];
@@ -424,23 +463,49 @@ __device__ __noinline__ void op_dispatch(Ctx& c, const Params& P, SolveOut* so) 
               out[a * s + cc] = 2.0 * h;
             };
             double sums[3] = {0, 0, 0};
-            row_pass<S, false>(c, P, U, s, P.p_up, P.p_lo, beta, theta_alpha_or_half(I, qt),
-                               is_theta(I) ? c.cs : nullptr, false, sums, epi);
+            if (is_pr(I)) {
+              pr_forward(P, c.t.rank, c.t.size, c.X, UPlain{U}, s);
+              c.t.sync();
+              pr_inverse<false>(P, c.t.rank, c.t.size, c.X, s, nullptr, P.p_up, beta, sums);
+              c.t.sync();
+              pr_combine(P, c.rl, c.rh, UPlain{U}, s, true, epi);
+            } else {
+              row_pass<S, false>(c, P, U, s, P.p_up, P.p_lo, beta, theta_alpha_or_half(I, qt),
+                                 is_theta(I) ? c.cs : nullptr, false, sums, epi);
+            }
             double v[4] = {hU, sums[0], sums[1], sums[2]};
             team_sum<4>(c.t, c.rs, v);
             break;
           }
           case 3: {  // map pass (FISTA T4 shape)
             double ms[2] = {0.0, 0.0};
-            map_pass<S>(c, P, U, s, kMapPR, P.p_up, nullptr, nullptr, ms);
+            if (is_pr(I)) {
+              pr_forward(P, c.t.rank, c.t.size, c.X, UPlain{U}, s);
+              c.t.sync();
+              pr_map_combine(P, c.kl, c.kh, s, [&](int64_t k, double d) {
+                const double r = d - I.b_up[k];
+                ms[0] = ms[0] + P.p_up[k] * r;
+                ms[1] = ms[1] + r * r;
+              });
+            } else {
+              map_pass<S>(c, P, U, s, kMapPR, P.p_up, nullptr, nullptr, ms);
+            }
             team_sum<2>(c.t, c.rs, ms);
             break;
           }
           case 4: {  // Lanczos matvec: fixed-q adjoint at s = 1 on column 0
             auto epi = [&](int64_t a, int, double h, double) { out[a] = -h; };
             double sums[3] = {0, 0, 0};
-            row_pass<1, true>(c, P, U, 1, P.p_up, P.p_lo, 0.0, theta_alpha_or_half(I, qt),
-                              is_theta(I) ? c.cs : nullptr, false, sums, epi);
+            if (is_pr(I)) {
+              pr_forward(P, c.t.rank, c.t.size, c.X, UPlain{U}, 1);
+              c.t.sync();
+              pr_inverse<true>(P, c.t.rank, c.t.size, c.X, 1, P.p_up, nullptr, 0.0, sums);
+              c.t.sync();
+              pr_combine(P, c.rl, c.rh, UPlain{U}, 1, true, epi);
+            } else {
+              row_pass<1, true>(c, P, U, 1, P.p_up, P.p_lo, 0.0, theta_alpha_or_half(I, qt),
+                                is_theta(I) ? c.cs : nullptr, false, sums, epi);
+            }
             c.t.sync();
             break;
           }

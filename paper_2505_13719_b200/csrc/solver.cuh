@@ -191,6 +191,15 @@ __device__ __forceinline__ void lz_apply(Ctx& c, const Params& P, const GOp& g, 
   };
   double sums[3] = {0.0, 0.0, 0.0};
   const double sumv = pv.sum;
+  if (is_pr(I)) {
+    const UScaled v{pv.src, pv.scale};
+    pr_forward(P, c.t.rank, c.t.size, c.X, v, 1);
+    c.t.sync();
+    pr_inverse<true>(P, c.t.rank, c.t.size, c.X, 1, g.qup, nullptr, 0.0, sums);
+    c.t.sync();
+    pr_combine(P, c.rl, c.rh, v, 1, true, epi);
+    return;
+  }
   row_pass_t<1, true>(c, P, UScaled{pv.src, pv.scale}, 1, g.qup, g.qlo, 0.0,
                       theta_alpha_or_half(I, g.qt), is_theta(I) ? &sumv : nullptr, false, sums,
                       epi);
@@ -408,6 +417,10 @@ __device__ __noinline__ bool lanczos_dev(Ctx& c, const Params& P, const GOp& g, 
   for (;;) {
     bool breakdown = false;
     while (filled < basis && matvecs < max_iters) {
+      if (c.t.xfailed) {
+        fail(c, kErrFabric, kMsgFabric);
+        return false;
+      }
       const int j = filled;
       w = slot_ptr(P, wslot[wc]);
       lz_apply(c, P, g, pend, w);  // materialises V(:, j) = pending column
@@ -588,7 +601,23 @@ __device__ __noinline__ bool gradop_dev(Ctx& c, const Params& P, const double* Y
   factor_stats<S>(c, P, Y, s, &ny2);
   double sums[2] = {0.0, 0.0};
   bool bad = false;
-  gradop_pass<S>(c, P, Y, s, beta, sums, &bad);
+  if (is_pr(I)) {
+    // GradientOperator (sdp_instance.cpp:73-83): residual = map - b, q = p + beta residual
+    pr_forward(P, c.t.rank, c.t.size, c.X, UPlain{Y}, s);
+    c.t.sync();
+    pr_map_combine(P, c.kl, c.kh, s, [&](int64_t k, double d) {
+      const double r = d - I.b_up[k];
+      const double pk = P.p_up[k];
+      const double q = pk + beta * r;
+      if (!isfinite(q)) bad = true;
+      P.r_up[k] = r;
+      P.q_up[k] = q;
+      sums[0] = sums[0] + pk * r;
+      sums[1] = sums[1] + r * r;
+    });
+  } else {
+    gradop_pass<S>(c, P, Y, s, beta, sums, &bad);
+  }
   double v[3] = {sums[0], sums[1], bad ? 1.0 : 0.0};
   team_sum<3>(c.t, c.rs, v);
   double p_r = v[0], r_r = v[1];
@@ -620,8 +649,16 @@ __device__ __noinline__ double fw_gap_dev(Ctx& c, const Params& P, const double*
   double gs = 0.0;
   auto epi = [&](int64_t, int, double h, double yo) { gs = gs + h * yo; };
   double sums[3] = {0.0, 0.0, 0.0};
-  row_pass<S, true>(c, P, Y, s, g.qup, g.qlo, 0.0, theta_alpha_or_half(I, g.qt),
-                    is_theta(I) ? c.cs : nullptr, false, sums, epi);
+  if (is_pr(I)) {
+    pr_forward(P, c.t.rank, c.t.size, c.X, UPlain{Y}, s);
+    c.t.sync();
+    pr_inverse<true>(P, c.t.rank, c.t.size, c.X, s, g.qup, nullptr, 0.0, sums);
+    c.t.sync();
+    pr_combine(P, c.rl, c.rh, UPlain{Y}, s, true, epi);
+  } else {
+    row_pass<S, true>(c, P, Y, s, g.qup, g.qlo, 0.0, theta_alpha_or_half(I, g.qt),
+                      is_theta(I) ? c.cs : nullptr, false, sums, epi);
+  }
   double v[1] = {gs};
   team_sum<1>(c.t, c.rs, v);
   return v[0];
@@ -665,6 +702,10 @@ __device__ __noinline__ bool hlr_dev(Ctx& c, const Params& P, Roles& R, int s, d
   const Cfg& cf = P.cfg;
   out = HlrOut();
   for (int step = 0;; ++step) {
+    if (c.t.xfailed) {
+      fail(c, kErrFabric, kMsgFabric);
+      return false;
+    }
     AippOut ao;
     bool ok = true;
     HALLAR_DISPATCH_S(s, ok = aipp_dev<S_>(c, P, R, s, eps_t, ao));
@@ -725,11 +766,24 @@ __device__ __noinline__ bool hlr_dev(Ctx& c, const Params& P, Roles& R, int s, d
       double v[2] = {0.0, 0.0};
       if (yv)
         for (int64_t a = c.rl + threadIdx.x; a < c.rh; a += kThreads) v[0] = v[0] + yv[a] * yv[a];
-      for (int64_t k = c.kl + threadIdx.x; k < c.kh; k += kThreads) {
-        const double d = yv ? yv[I.ei[k]] * yv[I.ej[k]] : 0.0;
-        const double bk = I.b_up ? I.b_up[k] : 0.0;
-        const double t = (P.r_up[k] + bk) - d;
-        v[1] = v[1] + t * t;
+      if (yv) publish_rows(c.t, yv, c.rl, c.rh, 1);
+      if (is_pr(I)) {
+        // A(yy') of the (n x 1) eigenvector; the spectrum cache is free here
+        if (yv) {
+          pr_forward(P, c.t.rank, c.t.size, c.X, UPlain{yv}, 1);
+          c.t.sync();
+        }
+        pr_map_combine(P, c.kl, c.kh, yv ? 1 : 0, [&](int64_t k, double d) {
+          const double t = (P.r_up[k] + I.b_up[k]) - d;
+          v[1] = v[1] + t * t;
+        });
+      } else {
+        for (int64_t k = c.kl + threadIdx.x; k < c.kh; k += kThreads) {
+          const double d = yv ? yv[I.ei[k]] * yv[I.ej[k]] : 0.0;
+          const double bk = I.b_up ? I.b_up[k] : 0.0;
+          const double t = (P.r_up[k] + bk) - d;
+          v[1] = v[1] + t * t;
+        }
       }
       team_sum<2>(c.t, c.rs, v);
       double sq = v[1];

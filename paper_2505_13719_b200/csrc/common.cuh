@@ -20,7 +20,9 @@ constexpr int kTileRows = 32;            // rows per row tile
 constexpr int kPrMaxNc = 8192;           // phase retrieval: transform length held in smem
 // shared scratch of one pass: the tile engine's arrays or one complex transform
 constexpr int kTileDoubles = kGroups * (5 * kTileEntries + 4 * (kTileRows + 1) + kTileEntries / 2);
-constexpr int kPassScratch = kTileDoubles > 2 * kPrMaxNc ? kTileDoubles : 2 * kPrMaxNc;
+constexpr int kPassScratch0 = kTileDoubles > 2 * kPrMaxNc ? kTileDoubles : 2 * kPrMaxNc;
+constexpr int kPassScratch = kPassScratch0;
+constexpr int kRtMinRows = 2 * kThreads; // rows per CTA from which the row-thread engine runs
 
 enum Family : int { kTheta = 0, kMatcomp = 1, kPhaseret = 2 };
 

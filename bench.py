@@ -137,6 +137,41 @@ def algorithmic_bytes_grad_pass(n, m_pairs, s):
     return 24 * m_pairs + 16 * n + 16 * n * s
 
 
+def large_roofline(H, np, peak, peak_kind, d=23, s=2, iters=10):
+    """In-kernel timing of the fused value+gradient pass (A(UU') and (C + A*(q))U,
+    one team pass) and of the constraint map on H(d,2), algorithmic bytes per
+    SURVEY §8(d) / DESIGN §3; traffic from the committed ncu capture."""
+    import time as _t
+    t0 = _t.perf_counter()
+    inst = H.build_theta_instance(H.make_hypercube(d))
+    gen = _t.perf_counter() - t0
+    rng = np.random.default_rng(0)
+    U = rng.standard_normal((inst.n, s))
+    U /= np.linalg.norm(U)
+    p = rng.standard_normal(inst.m)
+    npairs = inst.m - 1
+    out = {"instance": f"theta H({d},2): n={inst.n}, m={inst.m}, s={s}", "gen_s": round(gen, 2),
+           "peak": peak, "peak_kind": peak_kind, "unit": "GB/s", "bound": "hbm"}
+    ns = inst.bench_pass("grad_pass", U, p, beta=10.0, iters=iters)
+    alg = algorithmic_bytes_grad_pass(inst.n, npairs, s)
+    out["grad_pass"] = {"ns_per_pass": ns, "algorithmic_bytes": alg,
+                        "achieved": alg / (ns * 1e-9) / 1e9, "frac": alg / (ns * 1e-9) / 1e9 / peak}
+    ns = inst.bench_pass("map_pass", U, p, beta=10.0, iters=iters)
+    alg = 16 * npairs + 8 * inst.n * s
+    out["map_pass"] = {"ns_per_pass": ns, "algorithmic_bytes": alg,
+                       "achieved": alg / (ns * 1e-9) / 1e9, "frac": alg / (ns * 1e-9) / 1e9 / peak}
+    ns = inst.bench_pass("lanczos_matvec", U, p, beta=10.0, iters=iters)
+    alg = 24 * npairs + 32 * inst.n
+    out["lanczos_matvec"] = {"ns_per_pass": ns, "algorithmic_bytes": alg,
+                             "achieved": alg / (ns * 1e-9) / 1e9, "frac": alg / (ns * 1e-9) / 1e9 / peak}
+    tp = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tp):
+        with open(tp) as f:
+            out["grad_pass"]["traffic"] = json.load(f).get(f"grad_pass_H{d}_s{s}_bytes_per_pass")
+    del inst
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -144,6 +179,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-large", action="store_true", help="skip the H(23,2) pass roofline")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
@@ -234,7 +270,13 @@ def main():
     tp = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tp):
         with open(tp) as f:
-            traffic = json.load(f).get("grad_pass_H12_bytes_per_pass")
+            traffic = json.load(f).get(f"grad_pass_H12_s{s}_bytes_per_pass")
+
+    # the north-star instance (SURVEY §8 C5, H(23,2): n = 8.4M, m = 96.5M): the
+    # A / A* passes where HBM bandwidth, not latency, bounds them
+    large = None
+    if not args.no_large:
+        large = large_roofline(H, np, peak, peak_kind)
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -249,6 +291,7 @@ def main():
                      "kernel": "fused (C + A*(p+beta(A(UU')-b)))U row pass + reductions (one team pass)",
                      "algorithmic_bytes": alg, "ns_per_pass": ns, "peak_kind": peak_kind,
                      "team_sync_ns": ns_sync, "team_allreduce_ns": ns_red},
+        "roofline_c5": large,
         "clocks": clk,
         "wall_s_timed_region": wall,
         "counters": {"outer": reps[-1].outer_iters, "fista": reps[-1].fista_iters,

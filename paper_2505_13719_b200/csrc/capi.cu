@@ -30,6 +30,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   c.t.lrank = blockIdx.x;
   c.t.lsize = gridDim.x;
   c.t.fab = &P.fab;
+  c.t.mw = P.fab.world > 1;
   c.t.bar = P.bar;
   c.t.slots = P.slots;
   c.t.epoch = 0;
@@ -54,7 +55,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     c.vup = reinterpret_cast<int64_t*>(sm);
     sm += 2 * kGroups * (kTileRows + 1);
     c.tcol = reinterpret_cast<int32_t*>(sm);
-    sm = base + kPassScratch;
+    sm = base + P.pass_scratch;  // tile arrays (pairs) or one transform (phase retrieval)
   }
   c.cs = sm;
   sm += 2 * kSMax;
@@ -132,10 +133,13 @@ namespace {
 
 thread_local std::string g_err;
 
-constexpr size_t kSmemBytes =
-    sizeof(double) * (kWarps * kRedK + kRedK + kPassScratch + 2 * kSMax + kHLd * kHLd +
-                      3 * 32 * 32 + 4 * 32 + 64) +
-    sizeof(int) * 80;
+// dynamic shared memory: fixed solver state + the pass scratch of the family
+constexpr size_t smem_bytes(int pass_scratch) {
+  return sizeof(double) * (kWarps * kRedK + kRedK + pass_scratch + 2 * kSMax + kHLd * kHLd +
+                           3 * 32 * 32 + 4 * 32 + 64) +
+         sizeof(int) * 80;
+}
+constexpr size_t kSmemBytes = smem_bytes(kPassScratch);  // the largest (attribute, occupancy)
 
 struct CudaError : std::runtime_error {
   using std::runtime_error::runtime_error;
@@ -528,6 +532,7 @@ const char* msg_text(int id) {
 Params base_params(cuhallar_instance* in, const cuhallar_config* cfg) {
   Params P;
   P.I = in->I;
+  P.pass_scratch = in->h.family == kPhaseret ? int(std::max<int64_t>(2 * in->h.nc, 1024)) : kTileDoubles;
   cuhallar_config dc;
   cuhallar_config_default(&dc);
   P.cfg = to_dev_cfg(cfg ? *cfg : dc);
@@ -592,7 +597,7 @@ int launch(cuhallar_instance* in, Params& P, int grid, cudaStream_t st, SolveOut
     ck(cudaEventRecord(e0, st), "event");
   }
   ck(cudaLaunchCooperativeKernel((void*)hallar_kernel, dim3(grid), dim3(kThreads), args,
-                                 kSmemBytes, st),
+                                 smem_bytes(P.pass_scratch), st),
      "cooperative launch");
   if (ms) ck(cudaEventRecord(e1, st), "event");
   ck(cudaMemcpyAsync(so, in->dso, sizeof(SolveOut), cudaMemcpyDeviceToHost, st), "D2H out");
@@ -1160,7 +1165,7 @@ int cuhallar_solve_sharded(cuhallar_instance* const* insts, int world, const cuh
       SolveOut* dso = in->dso;
       void* args[] = {&Ps[r], &dso};
       ck(cudaLaunchCooperativeKernel((void*)hallar_kernel, dim3(G), dim3(kThreads), args,
-                                     kSmemBytes, st[r]),
+                                     smem_bytes(Ps[r].pass_scratch), st[r]),
          "cooperative launch (sharded)");
       ck(cudaEventRecord(e1[r], st[r]), "event");
     }

@@ -129,6 +129,7 @@ struct Params {
   int op = kOpSolve;
   DevPairs I;
   Cfg cfg;
+  int pass_scratch = 0;  // doubles of per-pass shared scratch in this launch
   // team
   Fabric fab;
   unsigned long long* bar = nullptr;

@@ -53,7 +53,8 @@ struct Team {
   unsigned long long xepoch = 0;
   bool xfailed = false;  // a rendezvous timed out (same value in every CTA of the rank)
 
-  __device__ __forceinline__ bool multi() const { return fab->world > 1; }
+  bool mw = false;  // world > 1 (cached: the fabric lives in parameter space)
+  __device__ __forceinline__ bool multi() const { return mw; }
 
   // barrier over the CTAs of this launch
   __device__ void lsync() {

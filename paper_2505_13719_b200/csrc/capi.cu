@@ -532,7 +532,9 @@ const char* msg_text(int id) {
 Params base_params(cuhallar_instance* in, const cuhallar_config* cfg) {
   Params P;
   P.I = in->I;
-  P.pass_scratch = in->h.family == kPhaseret ? int(std::max<int64_t>(2 * in->h.nc, 1024)) : kTileDoubles;
+  P.pass_scratch = in->h.family == kPhaseret
+                      ? int(std::max<int64_t>(2 * in->h.nc, 1024))
+                      : std::max(kTileDoubles, kRtTheta);  // fixed-q staging has no rhs
   cuhallar_config dc;
   cuhallar_config_default(&dc);
   P.cfg = to_dev_cfg(cfg ? *cfg : dc);

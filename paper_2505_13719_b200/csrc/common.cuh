@@ -23,6 +23,8 @@ constexpr int kTileDoubles = kGroups * (5 * kTileEntries + 4 * (kTileRows + 1) +
 constexpr int kPassScratch0 = kTileDoubles > 2 * kPrMaxNc ? kTileDoubles : 2 * kPrMaxNc;
 constexpr int kPassScratch = kPassScratch0;
 constexpr int kRtMinRows = 2 * kThreads; // rows per CTA from which the row-thread engine runs
+// fixed-q row-thread staging: col [2][8][threads] int32 + q [2][8][threads] f64
+constexpr int kRtTheta = 2 * 8 * kThreads / 2 + 2 * 8 * kThreads;
 
 enum Family : int { kTheta = 0, kMatcomp = 1, kPhaseret = 2 };
 

@@ -81,6 +81,14 @@ __global__ void __launch_bounds__(kThreads, 1)
   c.col = ip;
   ip += 40;
   c.jpq = ip;
+  ip += 40;
+  c.ccol = ip;
+  ip += kCacheEnt;
+  c.crlo = ip;
+  ip += kCacheRows + 1;
+  c.crup = ip;
+  ip += kCacheRows + 1;
+  c.ctr = ip;
   if (P.I.family == kPhaseret) {
     c.tl = c.th = 0;
     c.rl = P.I.n * c.t.rank / c.t.size;
@@ -90,6 +98,27 @@ __global__ void __launch_bounds__(kThreads, 1)
     c.th = P.I.ntiles * (c.t.rank + 1) / c.t.size;
     c.rl = P.I.tile_row[c.tl];
     c.rh = P.I.tile_row[c.th];
+  }
+  if (P.I.family != kPhaseret) {
+    // static structure of the CTA's rows -> shared memory (small instances)
+    const int64_t lo0 = P.I.lo_ptr[c.rl], up0 = P.I.up_ptr[c.rl];
+    const int64_t nlo = P.I.lo_ptr[c.rh] - lo0, nup = P.I.up_ptr[c.rh] - up0;
+    c.cached = c.th - c.tl <= kCacheTiles && c.rh - c.rl <= kCacheRows &&
+               nlo + nup <= kCacheEnt;
+    if (c.cached) {
+      c.clo0 = lo0;
+      c.cup0 = up0;
+      c.cnlo = (int32_t)nlo;
+      for (int64_t r = threadIdx.x; r <= c.rh - c.rl; r += kThreads) {
+        c.crlo[r] = (int32_t)(P.I.lo_ptr[c.rl + r] - lo0);
+        c.crup[r] = (int32_t)(P.I.up_ptr[c.rl + r] - up0);
+      }
+      for (int64_t t = threadIdx.x; t <= c.th - c.tl; t += kThreads)
+        c.ctr[t] = (int32_t)(P.I.tile_row[c.tl + t] - c.rl);
+      for (int64_t e = threadIdx.x; e < nlo; e += kThreads) c.ccol[e] = P.I.lo_col[lo0 + e];
+      for (int64_t e = threadIdx.x; e < nup; e += kThreads) c.ccol[nlo + e] = P.I.ej[up0 + e];
+    }
+    __syncthreads();
   }
   if (P.fab.world > 1) {
     // row-owner sharding: a CTA owns the upper (edge-order) entries of its rows
@@ -137,7 +166,7 @@ thread_local std::string g_err;
 constexpr size_t smem_bytes(int pass_scratch) {
   return sizeof(double) * (kWarps * kRedK + kRedK + pass_scratch + 2 * kSMax + kHLd * kHLd +
                            3 * 32 * 32 + 4 * 32 + 64) +
-         sizeof(int) * 80;
+         sizeof(int) * (80 + kCacheInts);
 }
 constexpr size_t kSmemBytes = smem_bytes(kPassScratch);  // the largest (attribute, occupancy)
 

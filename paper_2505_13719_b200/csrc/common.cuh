@@ -23,6 +23,13 @@ constexpr int kTileDoubles = kGroups * (5 * kTileEntries + 4 * (kTileRows + 1) +
 constexpr int kPassScratch0 = kTileDoubles > 2 * kPrMaxNc ? kTileDoubles : 2 * kPrMaxNc;
 constexpr int kPassScratch = kPassScratch0;
 constexpr int kRtMinRows = 2 * kThreads; // rows per CTA from which the row-thread engine runs
+// Small instances: a CTA's static structure (row pointers, tile starts and the
+// column index of every entry it folds) is cached in shared memory for the
+// whole launch, removing two dependent global round trips from every row pass.
+constexpr int kCacheEnt = 3072;          // entries (int32 columns)
+constexpr int kCacheRows = 1024;         // rows (+1 pointers, lower and upper)
+constexpr int kCacheTiles = 32;          // tiles (+1 starts)
+constexpr int kCacheInts = kCacheEnt + 2 * (kCacheRows + 1) + (kCacheTiles + 1) + 1;
 // fixed-q row-thread staging: col [2][8][threads] int32 + q [2][8][threads] f64
 constexpr int kRtTheta = 2 * 8 * kThreads / 2 + 2 * 8 * kThreads;
 

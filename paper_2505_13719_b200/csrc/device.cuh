@@ -45,6 +45,14 @@ struct Ctx {
   int32_t* tcol;  // [kTileEntries] gathered row per entry
   double* tterm;  // [kTileEntries * 4] w * U(b, c), c < 4
   double2* X;     // phase retrieval transform buffer (aliases the tile arrays)
+  // launch-long cache of the CTA's static pair structure (small instances)
+  bool cached = false;
+  int32_t* ccol;   // [kCacheEnt] lower columns of the CTA's rows, then upper columns
+  int32_t* crlo;   // [kCacheRows+1] lo_ptr[r] - lo_ptr[rl]
+  int32_t* crup;   // [kCacheRows+1] up_ptr[r] - up_ptr[rl]
+  int32_t* ctr;    // [kCacheTiles+1] tile_row[t] - rl
+  int64_t clo0 = 0, cup0 = 0;  // lo_ptr[rl], up_ptr[rl]
+  int32_t cnlo = 0;            // lower entries of the CTA's rows
   double* cs;     // [kSMax] column sums of the gathered factor (theta C-term)
   double* H;      // [kHLd][kHLd] Lanczos projected matrix (column-major)
   double* JA;     // [32*32] Jacobi work
@@ -443,6 +451,14 @@ __device__ __forceinline__ void row_pass_t(Ctx& c, const Params& P, const UA& U,
   // row pointers of `tile` -> buffer `buf` (visible after the next group_sync)
   auto load_ptrs = [&](int64_t tile, int buf) {
     if (tile < c.th) {
+      if (c.cached) {  // shared-memory copies of the static structure
+        const int q0 = c.ctr[tile - c.tl], q1 = c.ctr[tile - c.tl + 1];
+        if (gt <= q1 - q0) {
+          vlo(buf)[gt] = c.clo0 + c.crlo[q0 + gt];
+          vup(buf)[gt] = c.cup0 + c.crup[q0 + gt];
+        }
+        return;
+      }
       const int64_t q0 = __ldg(I.tile_row + tile), q1 = __ldg(I.tile_row + tile + 1);
       if (gt <= (int)(q1 - q0)) {
         vlo(buf)[gt] = __ldg(I.lo_ptr + q0 + gt);
@@ -488,7 +504,12 @@ __device__ __forceinline__ void row_pass_t(Ctx& c, const Params& P, const UA& U,
       const int32_t* cp = (B.up[e] ? I.ej : I.lo_col) + idxs[e];
       const double* pp = (B.up[e] ? Pup : Plo) + idxs[e];
       const double* bp = B.up[e] ? I.b_up : I.b_lo;
-      B.bcol[e] = __ldg(cp);
+      if (c.cached)
+        B.bcol[e] = B.ok[e] ? c.ccol[B.up[e] ? c.cnlo + (int)(idxs[e] - c.cup0)
+                                             : (int)(idxs[e] - c.clo0)]
+                            : 0;
+      else
+        B.bcol[e] = __ldg(cp);
       B.pq[e] = __ldg(pp);
       B.bb[e] = (!FIXED && bp) ? __ldg(bp + idxs[e]) : 0.0;
     }
@@ -989,9 +1010,10 @@ __device__ __forceinline__ double fista_a(double tau, double A, double L, double
 // holds y and buffers[v] holds v.
 //
 // Team passes per iteration (no L-doubling): T2 value+gradient at x~ (row
-// pass), T34 y+ and its map (y+ produced on the fly inside the map so no
-// separate barrier), T5 gradient at y+ fused with the x update and the NEXT
-// iteration's x~ and its statistics.  Three all-reduces per iteration.
+// pass), T34 y+ then the gradient row pass at y+ (its per-constraint dots give
+// al_value(y+); its fold is kept for T5), T5 an element-wise pass: gradient
+// at y+ from the kept fold, the x update and the NEXT iteration's x~ and its
+// statistics.  Two gather passes and three all-reduces per iteration.
 template <int S>
 __device__ __noinline__ bool fista_dev(Ctx& c, const Params& P, Roles& R, int s, double lambda,
                                        double L0, FistaOut& out) {
@@ -1001,9 +1023,6 @@ __device__ __noinline__ bool fista_dev(Ctx& c, const Params& P, Roles& R, int s,
   const double beta = c.beta;
   const double pt = c.p_trace;
   const bool theta = is_theta(I);
-  // y+ recomputed inside the map (saves a barrier) while the instance is
-  // latency-bound; beyond ~2^20 factor entries the divisions would dominate
-  const bool fuse_y = !is_pr(I) && !c.t.multi() && I.n * (int64_t)s <= (int64_t(1) << 20);
   double A = 0.0, tau = 1.0, L = L0;
   double* csx = c.cs + kSMax;  // column sums of x~ (kept apart from c.cs)
   prof_mark(c, P, kPfAipp);
@@ -1117,8 +1136,8 @@ __device__ __noinline__ bool fista_dev(Ctx& c, const Params& P, Roles& R, int s,
         nrmz = sqrt(zz);
       }
       const bool scale = !(nrmz <= 1.0);
-      // ---- T34: y+ (written for the row part, produced on the fly for the
-      //           map); ||y-W||^2, ||y-x~||^2, <g~, y-x~>, ||y||^2, colsum(y)
+      // ---- T34: y+ and ||y-W||^2, ||y-x~||^2, <g~, y-x~>, ||y||^2, colsum(y);
+      //           then the gradient row pass at y+ (al_value(y+) from its sums)
       {
         double* YN = P.buf[R.yn];
         double v3[4] = {0.0, 0.0, 0.0, 0.0};
@@ -1135,28 +1154,29 @@ __device__ __noinline__ bool fista_dev(Ctx& c, const Params& P, Roles& R, int s,
           v3[3] = v3[3] + y * y;
           return y;
         });
-        RowSrc src;
-        if (fuse_y) {
-          src.XT = XT;
-          src.GT = GT;
-          src.L = L;
-          src.nrm = nrmz;
-          src.scale = scale;
-        } else {
-          c.t.sync();  // y+ complete before it is gathered
-          src.U = YN;
-        }
+        // al_value(y+) needs A(y+ y+') only through sum p r and sum r^2, which the
+        // gradient row pass at y+ produces from the same per-constraint dots; the
+        // pass also leaves the adjoint fold of every row in HB, so the gradient at
+        // y+ (adap_fista.cpp:86) costs no second gather pass once y+ is accepted.
+        // Theta: the fold starts from zero and q_t y - colsum(y) is added in T5,
+        // when ||y+||^2 and colsum(y+) are known (tolerance-level reordering).
+        c.t.sync();  // y+ complete before it is gathered
+        double* HB = P.buf[kNBuf - 1];
         double ms[2] = {0.0, 0.0};
-        if (is_pr(I)) {
-          pr_forward(P, c.t.rank, c.t.size, c.X, UPlain{YN}, s);
-          c.t.sync();
-          pr_map_combine(P, c.kl, c.kh, s, [&](int64_t k, double d) {
-            const double r = d - I.b_up[k];
-            ms[0] = ms[0] + P.p_up[k] * r;
-            ms[1] = ms[1] + r * r;
-          });
-        } else {
-          map_pass_src<S>(c, P, src, s, kMapPR, P.p_up, nullptr, nullptr, ms);
+        {
+          double sums[3] = {0.0, 0.0, 0.0};
+          auto epi = [&](int64_t row, int cc, double h, double) { HB[row * s + cc] = h; };
+          if (is_pr(I)) {
+            pr_forward(P, c.t.rank, c.t.size, c.X, UPlain{YN}, s);
+            c.t.sync();
+            pr_inverse<false>(P, c.t.rank, c.t.size, c.X, s, nullptr, P.p_up, beta, sums);
+            c.t.sync();
+            pr_combine(P, c.rl, c.rh, UPlain{YN}, s, true, epi);
+          } else {
+            row_pass<S, false>(c, P, YN, s, P.p_up, P.p_lo, beta, 0.5, nullptr, theta, sums, epi);
+          }
+          ms[0] = sums[0];
+          ms[1] = sums[1];
         }
         double v[6] = {v3[0], v3[1], v3[2], v3[3], ms[0], ms[1]};
         stage_scalars<6>(c, v);
@@ -1244,15 +1264,26 @@ __device__ __noinline__ bool fista_dev(Ctx& c, const Params& P, Roles& R, int s,
           }
         }
       };
-      double sums[3] = {0.0, 0.0, 0.0};
-      if (is_pr(I)) {
-        // spectra of y+ are still cached from T34
-        pr_inverse<false>(P, c.t.rank, c.t.size, c.X, s, nullptr, P.p_up, beta, sums);
-        c.t.sync();
-        pr_combine(P, c.rl, c.rh, UPlain{YN}, s, true, epi);
+      // h(y+) = (C + A*(q(y+)))y+ was folded in T34 (HB); theta adds its C term
+      const double* HB = P.buf[kNBuf - 1];
+      if constexpr (S > 0) {
+        for (int64_t row = c.rl + threadIdx.x; row < c.rh; row += kThreads) {
+#pragma unroll
+          for (int k = 0; k < S; ++k) {
+            const int64_t o = row * S + k;
+            const double yo = YN[o];
+            const double h = theta ? (qt * yo - c.cs[k]) + HB[o] : HB[o];
+            epi(row, k, h, yo);
+          }
+        }
       } else {
-        row_pass<S, false>(c, P, YN, s, P.p_up, P.p_lo, beta, theta_alpha_or_half(I, qt),
-                           theta ? c.cs : nullptr, false, sums, epi);
+        for (int64_t row = c.rl + c.warp; row < c.rh; row += kWarps)
+          if (c.lane < s) {
+            const int64_t o = row * s + c.lane;
+            const double yo = YN[o];
+            const double h = theta ? (qt * yo - c.cs[c.lane]) + HB[o] : HB[o];
+            epi(row, c.lane, h, yo);
+          }
       }
       double v[3] = {vv, ddn, ntn};
       stage_scalars<3>(c, v);
@@ -1264,7 +1295,8 @@ __device__ __noinline__ bool fista_dev(Ctx& c, const Params& P, Roles& R, int s,
           if (c.lane == 0) c.rs.part[c.warp * kRedK + 3 + k] = x;
         }
       } else {
-        stage_colsums(c, s, 3, csn[0]);
+        // generic rank: lane c accumulated column c over the warp's rows
+        if (c.lane < s) c.rs.part[c.warp * kRedK + 3 + c.lane] = csn[0];
       }
       team_reduce_smem(c.t, c.rs, 3 + s);
       prof_mark(c, P, kPfT5);

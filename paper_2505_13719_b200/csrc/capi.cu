@@ -403,9 +403,7 @@ void ensure_workspace(cuhallar_instance* in, int grid, uint64_t seed, int block_
     in->dscal = dalloc<double>(8, &in->bytes);
     in->discal = dalloc<int>(8, &in->bytes);
     in->dso = dalloc<SolveOut>(1, &in->bytes);
-    ck(cudaHostAlloc(&in->trace_host, sizeof(TraceEv) * in->trace_cap, cudaHostAllocMapped),
-       "trace ring");
-    ck(cudaHostAlloc(&in->trace_count_host, sizeof(int), cudaHostAllocMapped), "trace count");
+
   }
   if (grid > in->ws_grid) {
     if (in->slots) cudaFree(in->slots);
@@ -416,7 +414,9 @@ void ensure_workspace(cuhallar_instance* in, int grid, uint64_t seed, int block_
   if (seed != in->lz_seed) {
     // Lanczos start vector + breakdown refills: the stream of
     // gaussian_vector(n, Rng(seed ^ 0x9b97f4a7c15)) calls (lanczos.cpp:46-50, 128-129)
-    const int refill = int(std::max<int64_t>(2, std::min<int64_t>(64, (int64_t(1) << 24) / n)));
+    // (a refill is drawn only when a Krylov basis breaks down before reaching n:
+    // rare, so a few per call suffice beyond tiny instances)
+    const int refill = int(std::max<int64_t>(4, std::min<int64_t>(64, (int64_t(1) << 16) / n)));
     const auto v = hh::gaussian_stream(seed ^ 0x9b97f4a7c15ULL, n * (1 + refill));
     if (in->lz_rand) cudaFree(in->lz_rand);
     in->lz_rand = dupload(v, &in->bytes);
@@ -993,6 +993,11 @@ int cuhallar_solve(cuhallar_instance* in, const cuhallar_config* cfg, const doub
     const int grid = grid_size(cfg->team_ctas);
     ensure_workspace(in, grid, cfg->seed, cfg->eig_block_restart);
     const int s = upload_start(in, cfg, U0_host, s0);
+    if (cfg->trace && !in->trace_host) {  // TraceEvent ring, mapped host memory (lazy)
+      ck(cudaHostAlloc(&in->trace_host, sizeof(TraceEv) * in->trace_cap, cudaHostAllocMapped),
+         "trace ring");
+      ck(cudaHostAlloc(&in->trace_count_host, sizeof(int), cudaHostAllocMapped), "trace count");
+    }
     Params P = base_params(in, cfg);
     P.op = kOpSolve;
     P.s_in = s;
@@ -1058,7 +1063,7 @@ static int fill_report(cuhallar_instance* in, const SolveOut& so, float ms, doub
     rep->device_seconds = ms * 1e-3;
     rep->tau = tau;
     rep->theta = so.theta;
-    rep->trace_dropped = std::max(0, *in->trace_count_host - in->trace_cap);
+    rep->trace_dropped = in->trace_count_host ? std::max(0, *in->trace_count_host - in->trace_cap) : 0;
     std::snprintf(rep->message, sizeof(rep->message), "%s", msg_text(so.msg));
     if (sol) {
       auto S = std::make_unique<cuhallar_solution>();

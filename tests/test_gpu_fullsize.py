@@ -9,6 +9,8 @@ properties (the oracle cannot run these in seconds):
   (test_instances.cpp:27-41 at scale);
 * fused == split: C_plus_adjoint(q, U) == apply_C(U) + apply_adjoint(q, U) to
   1e-12 (the fused form accumulates onto C U, as the reference does);
+* al_gradient (q formed on the fly) == 2 C_plus_adjoint(p + beta (A(UU') - b), U)
+  bit for bit;
 * the instance itself: edge set of H(23,2) equals make_hypercube's
   (v, v ^ 2^bit) rule; MC sample count equals matcomp_constraint_count.
 Both instances take several GB of HBM and tens of seconds to build."""
@@ -45,6 +47,13 @@ def _check_operator_properties(inst, U, i, j, trace, rng):
     lhs = float(out @ p)
     rhs = float(np.sum(adj * U))
     assert abs(lhs - rhs) <= 1e-10 * max(1.0, abs(lhs))
+    # al_gradient forms q = p + beta (A(UU') - b) on the fly (row pass with
+    # per-entry dots); the same q through the map and C_plus_adjoint must give
+    # the bit-identical gradient 2 (C + A*(q))U (sdp_instance.cpp:62-71)
+    beta = 3.0
+    q = p + beta * (out - inst.b)
+    grad = inst.al_gradient(U, p, beta)
+    assert np.array_equal(grad, 2.0 * inst.C_plus_adjoint(q, U))
     fused = inst.C_plus_adjoint(p, U)
     split = inst.apply_C(U) + adj
     # the fused form accumulates onto C U (the reference's apply_C_plus_adjoint

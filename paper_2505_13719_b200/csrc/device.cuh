@@ -321,7 +321,7 @@ __device__ __forceinline__ void row_pass_rt_async(Ctx& c, const Params& P, const
 
 // ------------------------------------------------- row-thread engine ------
 // Large instances (many rows per CTA), ranks 1..4: one thread owns a whole
-// row and walks its lower then upper entries — increasing constraint k, the
+// row and walks its lower then upper entries as one stream — increasing k, the
 // reference's adjoint_into order (instances.cpp:45-52) — with the column
 // accumulators in registers.  Entries are taken in batches of B: the B
 // column indices and multipliers (contiguous per row) are loaded first, then
@@ -337,7 +337,7 @@ __device__ __forceinline__ void row_pass_rt(Ctx& c, const Params& P, const UA& U
                                             double alpha, const double* cs, bool zero_init,
                                             double (&sums)[3], Epi& epi) {
   static_assert(S >= 1 && S <= 4, "row-thread engine: ranks 1..4");
-  constexpr int B = S <= 2 ? 8 : 4;
+  constexpr int B = S <= 3 ? 8 : 4;
   const DevPairs& I = P.I;
   const bool has_b = !FIXED && I.b_up != nullptr;
   double csr[S];
@@ -354,56 +354,55 @@ __device__ __forceinline__ void row_pass_rt(Ctx& c, const Params& P, const UA& U
         if (cs) acc[k] = acc[k] - csr[k];
       }
     }
+    // the row's entries as one stream: lower entries, then upper (increasing k)
+    const int64_t lo0 = __ldg(I.lo_ptr + a), up0 = __ldg(I.up_ptr + a);
+    const int nlo = (int)(__ldg(I.lo_ptr + a + 1) - lo0);
+    const int nv = nlo + (int)(__ldg(I.up_ptr + a + 1) - up0);
 #pragma unroll 1
-    for (int part = 0; part < 2; ++part) {
-      const bool upper = part == 1;
-      const int64_t e0 = upper ? __ldg(I.up_ptr + a) : __ldg(I.lo_ptr + a);
-      const int64_t e1 = upper ? __ldg(I.up_ptr + a + 1) : __ldg(I.lo_ptr + a + 1);
-      const int32_t* __restrict__ colp = upper ? I.ej : I.lo_col;
-      const double* __restrict__ pp = upper ? Pup : Plo;
-      const double* __restrict__ bp = upper ? I.b_up : I.b_lo;
-#pragma unroll 1
-      for (int64_t e = e0; e < e1; e += B) {
-        int64_t bc[B];
-        double pk[B], bk[B];
+    for (int v0 = 0; v0 < nv; v0 += B) {
+      int64_t bc[B];
+      double pk[B], bk[B];
 #pragma unroll
-        for (int u = 0; u < B; ++u) {
-          const bool ok = e + u < e1;
-          bc[u] = ok ? (int64_t)__ldg(colp + e + u) : a;
-          pk[u] = ok ? __ldg(pp + e + u) : 0.0;
-          bk[u] = (ok && has_b) ? __ldg(bp + e + u) : 0.0;
-        }
-        double ub[B][S];
+      for (int u = 0; u < B; ++u) {
+        const int v = v0 + u;
+        const bool ok = v < nv;
+        const bool up = v >= nlo;
+        const int64_t e = up ? up0 + (v - nlo) : lo0 + v;
+        bc[u] = ok ? (int64_t)__ldg((up ? I.ej : I.lo_col) + e) : a;
+        pk[u] = ok ? __ldg((up ? Pup : Plo) + e) : 0.0;
+        bk[u] = (ok && has_b) ? __ldg((up ? I.b_up : I.b_lo) + e) : 0.0;
+      }
+      double ub[B][S];
 #pragma unroll
-        for (int u = 0; u < B; ++u)
+      for (int u = 0; u < B; ++u)
 #pragma unroll
-          for (int k = 0; k < S; ++k) ub[u][k] = U(bc[u] * S + k);
+        for (int k = 0; k < S; ++k) ub[u][k] = U(bc[u] * S + k);
 #pragma unroll
-        for (int u = 0; u < B; ++u) {
-          if (e + u >= e1) break;
-          double w;
-          if (FIXED) {
-            w = 0.5 * pk[u];
-          } else {
-            double d = 0.0;
+      for (int u = 0; u < B; ++u) {
+        const int v = v0 + u;
+        if (v >= nv) break;
+        double w;
+        if (FIXED) {
+          w = 0.5 * pk[u];
+        } else {
+          double d = 0.0;
 #pragma unroll
-            for (int k = 0; k < S; ++k) {
-              const double t = ua[k] * ub[u][k];
-              d = (k == 0) ? t : d + t;
-            }
-            const double rr = d - bk[u];
-            const double q = pk[u] + beta * rr;
-            w = 0.5 * q;
-            if (upper) {
-              sums[0] = sums[0] + pk[u] * rr;
-              sums[1] = sums[1] + rr * rr;
-              sums[2] = sums[2] + q * (rr + bk[u]);
-            }
+          for (int k = 0; k < S; ++k) {
+            const double t = ua[k] * ub[u][k];
+            d = (k == 0) ? t : d + t;
           }
-          // skipped terms (w == 0, instances.cpp:47): x + (-0.0) == x exactly
-#pragma unroll
-          for (int k = 0; k < S; ++k) acc[k] = acc[k] + ((w != 0.0) ? w * ub[u][k] : -0.0);
+          const double rr = d - bk[u];
+          const double q = pk[u] + beta * rr;
+          w = 0.5 * q;
+          if (v >= nlo) {  // upper entry: each constraint counted once
+            sums[0] = sums[0] + pk[u] * rr;
+            sums[1] = sums[1] + rr * rr;
+            sums[2] = sums[2] + q * (rr + bk[u]);
+          }
         }
+        // skipped terms (w == 0, instances.cpp:47): x + (-0.0) == x exactly
+#pragma unroll
+        for (int k = 0; k < S; ++k) acc[k] = acc[k] + ((w != 0.0) ? w * ub[u][k] : -0.0);
       }
     }
 #pragma unroll

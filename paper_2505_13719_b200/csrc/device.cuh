@@ -321,7 +321,7 @@ __device__ __forceinline__ void row_pass_rt_async(Ctx& c, const Params& P, const
 
 // ------------------------------------------------- row-thread engine ------
 // Large instances (many rows per CTA), ranks 1..4: one thread owns a whole
-// row and walks its lower then upper entries as one stream — increasing k, the
+// row and walks its lower then upper entries — increasing constraint k, the
 // reference's adjoint_into order (instances.cpp:45-52) — with the column
 // accumulators in registers.  Entries are taken in batches of B: the B
 // column indices and multipliers (contiguous per row) are loaded first, then
@@ -337,7 +337,7 @@ __device__ __forceinline__ void row_pass_rt(Ctx& c, const Params& P, const UA& U
                                             double alpha, const double* cs, bool zero_init,
                                             double (&sums)[3], Epi& epi) {
   static_assert(S >= 1 && S <= 4, "row-thread engine: ranks 1..4");
-  constexpr int B = S <= 3 ? 8 : 4;
+  constexpr int B = S <= 2 ? 8 : 4;
   const DevPairs& I = P.I;
   const bool has_b = !FIXED && I.b_up != nullptr;
   double csr[S];
@@ -354,55 +354,56 @@ __device__ __forceinline__ void row_pass_rt(Ctx& c, const Params& P, const UA& U
         if (cs) acc[k] = acc[k] - csr[k];
       }
     }
-    // the row's entries as one stream: lower entries, then upper (increasing k)
-    const int64_t lo0 = __ldg(I.lo_ptr + a), up0 = __ldg(I.up_ptr + a);
-    const int nlo = (int)(__ldg(I.lo_ptr + a + 1) - lo0);
-    const int nv = nlo + (int)(__ldg(I.up_ptr + a + 1) - up0);
 #pragma unroll 1
-    for (int v0 = 0; v0 < nv; v0 += B) {
-      int64_t bc[B];
-      double pk[B], bk[B];
+    for (int part = 0; part < 2; ++part) {
+      const bool upper = part == 1;
+      const int64_t e0 = upper ? __ldg(I.up_ptr + a) : __ldg(I.lo_ptr + a);
+      const int64_t e1 = upper ? __ldg(I.up_ptr + a + 1) : __ldg(I.lo_ptr + a + 1);
+      const int32_t* __restrict__ colp = upper ? I.ej : I.lo_col;
+      const double* __restrict__ pp = upper ? Pup : Plo;
+      const double* __restrict__ bp = upper ? I.b_up : I.b_lo;
+#pragma unroll 1
+      for (int64_t e = e0; e < e1; e += B) {
+        int64_t bc[B];
+        double pk[B], bk[B];
 #pragma unroll
-      for (int u = 0; u < B; ++u) {
-        const int v = v0 + u;
-        const bool ok = v < nv;
-        const bool up = v >= nlo;
-        const int64_t e = up ? up0 + (v - nlo) : lo0 + v;
-        bc[u] = ok ? (int64_t)__ldg((up ? I.ej : I.lo_col) + e) : a;
-        pk[u] = ok ? __ldg((up ? Pup : Plo) + e) : 0.0;
-        bk[u] = (ok && has_b) ? __ldg((up ? I.b_up : I.b_lo) + e) : 0.0;
-      }
-      double ub[B][S];
-#pragma unroll
-      for (int u = 0; u < B; ++u)
-#pragma unroll
-        for (int k = 0; k < S; ++k) ub[u][k] = U(bc[u] * S + k);
-#pragma unroll
-      for (int u = 0; u < B; ++u) {
-        const int v = v0 + u;
-        if (v >= nv) break;
-        double w;
-        if (FIXED) {
-          w = 0.5 * pk[u];
-        } else {
-          double d = 0.0;
-#pragma unroll
-          for (int k = 0; k < S; ++k) {
-            const double t = ua[k] * ub[u][k];
-            d = (k == 0) ? t : d + t;
-          }
-          const double rr = d - bk[u];
-          const double q = pk[u] + beta * rr;
-          w = 0.5 * q;
-          if (v >= nlo) {  // upper entry: each constraint counted once
-            sums[0] = sums[0] + pk[u] * rr;
-            sums[1] = sums[1] + rr * rr;
-            sums[2] = sums[2] + q * (rr + bk[u]);
-          }
+        for (int u = 0; u < B; ++u) {
+          const bool ok = e + u < e1;
+          bc[u] = ok ? (int64_t)__ldg(colp + e + u) : a;
+          pk[u] = ok ? __ldg(pp + e + u) : 0.0;
+          bk[u] = (ok && has_b) ? __ldg(bp + e + u) : 0.0;
         }
-        // skipped terms (w == 0, instances.cpp:47): x + (-0.0) == x exactly
+        double ub[B][S];
 #pragma unroll
-        for (int k = 0; k < S; ++k) acc[k] = acc[k] + ((w != 0.0) ? w * ub[u][k] : -0.0);
+        for (int u = 0; u < B; ++u)
+#pragma unroll
+          for (int k = 0; k < S; ++k) ub[u][k] = U(bc[u] * S + k);
+#pragma unroll
+        for (int u = 0; u < B; ++u) {
+          if (e + u >= e1) break;
+          double w;
+          if (FIXED) {
+            w = 0.5 * pk[u];
+          } else {
+            double d = 0.0;
+#pragma unroll
+            for (int k = 0; k < S; ++k) {
+              const double t = ua[k] * ub[u][k];
+              d = (k == 0) ? t : d + t;
+            }
+            const double rr = d - bk[u];
+            const double q = pk[u] + beta * rr;
+            w = 0.5 * q;
+            if (upper) {
+              sums[0] = sums[0] + pk[u] * rr;
+              sums[1] = sums[1] + rr * rr;
+              sums[2] = sums[2] + q * (rr + bk[u]);
+            }
+          }
+          // skipped terms (w == 0, instances.cpp:47): x + (-0.0) == x exactly
+#pragma unroll
+          for (int k = 0; k < S; ++k) acc[k] = acc[k] + ((w != 0.0) ? w * ub[u][k] : -0.0);
+        }
       }
     }
 #pragma unroll
@@ -1009,10 +1010,9 @@ __device__ __forceinline__ double fista_a(double tau, double A, double L, double
 // holds y and buffers[v] holds v.
 //
 // Team passes per iteration (no L-doubling): T2 value+gradient at x~ (row
-// pass), T34 y+ then the gradient row pass at y+ (its per-constraint dots give
-// al_value(y+); its fold is kept for T5), T5 an element-wise pass: gradient
-// at y+ from the kept fold, the x update and the NEXT iteration's x~ and its
-// statistics.  Two gather passes and three all-reduces per iteration.
+// pass), T34 y+ and its map (y+ produced on the fly inside the map so no
+// separate barrier), T5 gradient at y+ fused with the x update and the NEXT
+// iteration's x~ and its statistics.  Three all-reduces per iteration.
 template <int S>
 __device__ __noinline__ bool fista_dev(Ctx& c, const Params& P, Roles& R, int s, double lambda,
                                        double L0, FistaOut& out) {
@@ -1022,6 +1022,9 @@ __device__ __noinline__ bool fista_dev(Ctx& c, const Params& P, Roles& R, int s,
   const double beta = c.beta;
   const double pt = c.p_trace;
   const bool theta = is_theta(I);
+  // y+ recomputed inside the map (saves a barrier) while the instance is
+  // latency-bound; beyond ~2^20 factor entries the divisions would dominate
+  const bool fuse_y = !is_pr(I) && !c.t.multi() && I.n * (int64_t)s <= (int64_t(1) << 20);
   double A = 0.0, tau = 1.0, L = L0;
   double* csx = c.cs + kSMax;  // column sums of x~ (kept apart from c.cs)
   prof_mark(c, P, kPfAipp);
@@ -1135,8 +1138,8 @@ __device__ __noinline__ bool fista_dev(Ctx& c, const Params& P, Roles& R, int s,
         nrmz = sqrt(zz);
       }
       const bool scale = !(nrmz <= 1.0);
-      // ---- T34: y+ and ||y-W||^2, ||y-x~||^2, <g~, y-x~>, ||y||^2, colsum(y);
-      //           then the gradient row pass at y+ (al_value(y+) from its sums)
+      // ---- T34: y+ (written for the row part, produced on the fly for the
+      //           map); ||y-W||^2, ||y-x~||^2, <g~, y-x~>, ||y||^2, colsum(y)
       {
         double* YN = P.buf[R.yn];
         double v3[4] = {0.0, 0.0, 0.0, 0.0};
@@ -1153,29 +1156,28 @@ __device__ __noinline__ bool fista_dev(Ctx& c, const Params& P, Roles& R, int s,
           v3[3] = v3[3] + y * y;
           return y;
         });
-        // al_value(y+) needs A(y+ y+') only through sum p r and sum r^2, which the
-        // gradient row pass at y+ produces from the same per-constraint dots; the
-        // pass also leaves the adjoint fold of every row in HB, so the gradient at
-        // y+ (adap_fista.cpp:86) costs no second gather pass once y+ is accepted.
-        // Theta: the fold starts from zero and q_t y - colsum(y) is added in T5,
-        // when ||y+||^2 and colsum(y+) are known (tolerance-level reordering).
-        c.t.sync();  // y+ complete before it is gathered
-        double* HB = P.buf[kNBuf - 1];
+        RowSrc src;
+        if (fuse_y) {
+          src.XT = XT;
+          src.GT = GT;
+          src.L = L;
+          src.nrm = nrmz;
+          src.scale = scale;
+        } else {
+          c.t.sync();  // y+ complete before it is gathered
+          src.U = YN;
+        }
         double ms[2] = {0.0, 0.0};
-        {
-          double sums[3] = {0.0, 0.0, 0.0};
-          auto epi = [&](int64_t row, int cc, double h, double) { HB[row * s + cc] = h; };
-          if (is_pr(I)) {
-            pr_forward(P, c.t.rank, c.t.size, c.X, UPlain{YN}, s);
-            c.t.sync();
-            pr_inverse<false>(P, c.t.rank, c.t.size, c.X, s, nullptr, P.p_up, beta, sums);
-            c.t.sync();
-            pr_combine(P, c.rl, c.rh, UPlain{YN}, s, true, epi);
-          } else {
-            row_pass<S, false>(c, P, YN, s, P.p_up, P.p_lo, beta, 0.5, nullptr, theta, sums, epi);
-          }
-          ms[0] = sums[0];
-          ms[1] = sums[1];
+        if (is_pr(I)) {
+          pr_forward(P, c.t.rank, c.t.size, c.X, UPlain{YN}, s);
+          c.t.sync();
+          pr_map_combine(P, c.kl, c.kh, s, [&](int64_t k, double d) {
+            const double r = d - I.b_up[k];
+            ms[0] = ms[0] + P.p_up[k] * r;
+            ms[1] = ms[1] + r * r;
+          });
+        } else {
+          map_pass_src<S>(c, P, src, s, kMapPR, P.p_up, nullptr, nullptr, ms);
         }
         double v[6] = {v3[0], v3[1], v3[2], v3[3], ms[0], ms[1]};
         stage_scalars<6>(c, v);
@@ -1263,26 +1265,15 @@ __device__ __noinline__ bool fista_dev(Ctx& c, const Params& P, Roles& R, int s,
           }
         }
       };
-      // h(y+) = (C + A*(q(y+)))y+ was folded in T34 (HB); theta adds its C term
-      const double* HB = P.buf[kNBuf - 1];
-      if constexpr (S > 0) {
-        for (int64_t row = c.rl + threadIdx.x; row < c.rh; row += kThreads) {
-#pragma unroll
-          for (int k = 0; k < S; ++k) {
-            const int64_t o = row * S + k;
-            const double yo = YN[o];
-            const double h = theta ? (qt * yo - c.cs[k]) + HB[o] : HB[o];
-            epi(row, k, h, yo);
-          }
-        }
+      double sums[3] = {0.0, 0.0, 0.0};
+      if (is_pr(I)) {
+        // spectra of y+ are still cached from T34
+        pr_inverse<false>(P, c.t.rank, c.t.size, c.X, s, nullptr, P.p_up, beta, sums);
+        c.t.sync();
+        pr_combine(P, c.rl, c.rh, UPlain{YN}, s, true, epi);
       } else {
-        for (int64_t row = c.rl + c.warp; row < c.rh; row += kWarps)
-          if (c.lane < s) {
-            const int64_t o = row * s + c.lane;
-            const double yo = YN[o];
-            const double h = theta ? (qt * yo - c.cs[c.lane]) + HB[o] : HB[o];
-            epi(row, c.lane, h, yo);
-          }
+        row_pass<S, false>(c, P, YN, s, P.p_up, P.p_lo, beta, theta_alpha_or_half(I, qt),
+                           theta ? c.cs : nullptr, false, sums, epi);
       }
       double v[3] = {vv, ddn, ntn};
       stage_scalars<3>(c, v);
@@ -1294,8 +1285,7 @@ __device__ __noinline__ bool fista_dev(Ctx& c, const Params& P, Roles& R, int s,
           if (c.lane == 0) c.rs.part[c.warp * kRedK + 3 + k] = x;
         }
       } else {
-        // generic rank: lane c accumulated column c over the warp's rows
-        if (c.lane < s) c.rs.part[c.warp * kRedK + 3 + c.lane] = csn[0];
+        stage_colsums(c, s, 3, csn[0]);
       }
       team_reduce_smem(c.t, c.rs, 3 + s);
       prof_mark(c, P, kPfT5);

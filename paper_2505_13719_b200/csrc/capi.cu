@@ -945,6 +945,11 @@ static void host_factor_to_buf0(cuhallar_instance* in, const double* U_host, int
 }
 static double host_multiplier_to_dev(cuhallar_instance* in, const double* p_host) {
   const int64_t np = in->h.np;
+  if (!p_host) {  // cold start p0 = 0 (solver.cpp:126-134): no host staging
+    ck(cudaMemset(in->p_up, 0, np * sizeof(double)), "p_up");
+    ck(cudaMemset(in->p_lo, 0, np * sizeof(double)), "p_lo");
+    return 0.0;
+  }
   std::vector<double> up(np), lo(np);
   for (int64_t k = 0; k < np; ++k) up[k] = p_host ? p_host[k] : 0.0;
   if (in->h.family != kPhaseret)

@@ -685,8 +685,6 @@ cuhallar_instance* finish_pairs(hh::HostInst&& h) {
   return in.release();
 }
 
-void check_pairs(const cuhallar_instance*) {}
-
 // gen_phase_retrieval (instances.cpp:298-389): masks, twiddles and the
 // spectrum / adjoint scratch go to HBM; b = map of the hidden signal is
 // computed by the device operator itself (instances.cpp:323-328).
@@ -858,7 +856,6 @@ static int run_op(cuhallar_instance* in, int op, const double* U_dev, int64_t ld
                   const double* vec_dev, double beta, double* out_vec, double* out_mat,
                   int64_t ldo, double* val_host, cudaStream_t st) {
   return guard([&] {
-    check_pairs(in);
     DevGuard dg(in->device);
     if (s < 1 || s > kSMax) throw hh::InputError("factor rank must be in [1, 32]");
     if (ldu < in->h.n) throw hh::InputError("leading dimension < n");
@@ -989,7 +986,6 @@ int cuhallar_solve(cuhallar_instance* in, const cuhallar_config* cfg, const doub
                    int s0, const double* p0_host, cuhallar_report* rep, cuhallar_solution** sol,
                    cuhallar_trace_fn fn, void* user) {
   return guard([&] {
-    check_pairs(in);
     DevGuard dg(in->device);
     validate_cfg(*cfg);
     std::lock_guard<std::mutex> lk(in->mu);
@@ -1263,7 +1259,6 @@ int cuhallar_min_eig_gradient(cuhallar_instance* in, const double* U_host, int s
                               int block_restart, uint64_t seed, double* lambda, double* v_host,
                               double* residual, int* matvecs, int* converged) {
   return guard([&] {
-    check_pairs(in);
     DevGuard dg(in->device);
     if (s < 1 || s > kSMax) throw hh::InputError("factor rank must be in [1, 32]");
     if (block_restart < 2 || block_restart > kLanczosMax)
@@ -1306,7 +1301,6 @@ int cuhallar_aipp(cuhallar_instance* in, const double* p_host, double beta, cons
                   int* prox_iters, int* fista_iters, double* R_norm, double* g_value,
                   double* lambda) {
   return guard([&] {
-    check_pairs(in);
     DevGuard dg(in->device);
     if (s < 1 || s > kSMax) throw hh::InputError("factor rank must be in [1, 32]");
     std::lock_guard<std::mutex> lk(in->mu);
@@ -1347,7 +1341,6 @@ int cuhallar_bench_pass(cuhallar_instance* in, int kind, const double* U_host, i
                         const double* p_host, double beta, int iters, int team_ctas,
                         double* ns_per_pass) {
   return guard([&] {
-    check_pairs(in);
     DevGuard dg(in->device);
     if (s < 1 || s > kSMax) throw hh::InputError("factor rank must be in [1, 32]");
     std::lock_guard<std::mutex> lk(in->mu);

@@ -66,6 +66,14 @@ int cuhallar_theta_file(const char* path, int fmt, cuhallar_instance** out);
 int cuhallar_gen_matrix_completion(int64_t n1, int64_t n2, int r, uint64_t seed,
                                    int offset_sample_count, double tau_safety,
                                    cuhallar_instance** out);
+/* Matrix completion with the paper's sampling rule (
+ * no reference counterpart — the reference draws m = matcomp_constraint_count
+ * distinct entries, instances.cpp:123-159): `draws` (i, j) draws with replacement
+ * from the same Rng stream after the hidden factors, deduplicated and sorted.
+ * The paper's tables use draws = 40 (n1 + n2). */
+int cuhallar_gen_matrix_completion_paper(int64_t n1, int64_t n2, int r, uint64_t seed,
+                                         int64_t draws, double tau_safety,
+                                         cuhallar_instance** out);
 /* matcomp_constraint_count  instances.cpp:123-129 */
 int64_t cuhallar_matcomp_constraint_count(int64_t n1, int64_t n2, int r, int offset);
 /* gen_phase_retrieval(PrSpec)  instances.cpp:239-389 */

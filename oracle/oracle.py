@@ -200,6 +200,16 @@ class OracleInstance:
         return cls(h.value)
 
     @classmethod
+    def matcomp_paper(cls, n1, n2, r, seed=0, draws_per_dim=40, tau_safety=1.2):
+        """The paper's sampling rule (draws_per_dim * (n1 + n2) draws with
+        replacement, deduplicated) — SURVEY §8(f) row 2; not in the reference."""
+        h = _vp()
+        _check(lib().orc_matcomp_paper(C.c_longlong(n1), C.c_longlong(n2), C.c_int(r), C.c_ulonglong(seed),
+                                       C.c_longlong(draws_per_dim * (n1 + n2)), C.c_double(tau_safety),
+                                       C.byref(h)))
+        return cls(h.value)
+
+    @classmethod
     def phaseret(cls, n, L, seed=0, tau_slack=1.1):
         h = _vp()
         _check(lib().orc_phaseret(C.c_longlong(n), C.c_int(L), C.c_ulonglong(seed),

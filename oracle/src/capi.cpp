@@ -123,6 +123,19 @@ int orc_matcomp(long long n1, long long n2, int r, unsigned long long seed, int 
     *out = h;
   });
 }
+int orc_matcomp_paper(long long n1, long long n2, int r, unsigned long long seed,
+                      long long draws, double tau_safety, void** out) {
+  return guard([&] {
+    McData d = matrix_completion(n1, n2, r, seed, false, tau_safety, draws);
+    auto* h = new Handle;
+    h->inst = std::move(d.inst);
+    h->family = 1;
+    h->oi = std::move(d.omega_i);
+    h->oj = std::move(d.omega_j);
+    h->nuclear = d.nuclear_norm;
+    *out = h;
+  });
+}
 long long orc_matcomp_count(long long n1, long long n2, int r, int offset) {
   return mc_count(n1, n2, r, offset != 0);
 }

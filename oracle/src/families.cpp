@@ -218,22 +218,35 @@ Vec singular_values(Mat A) {
 }
 }  // namespace
 
-// instances.cpp:131-234
+// instances.cpp:131-234.  paper_draws > 0 selects the paper's sampling rule
+// instead (not in the reference): that many
+// (i, j) draws with replacement from the same stream, then deduplicated.
 McData matrix_completion(i64 n1, i64 n2, int r, u64 seed, bool offset,
-                         double tau_safety) {
+                         double tau_safety, i64 paper_draws) {
   need(n1 >= 1 && n2 >= n1, "matcomp: need n2 >= n1 >= 1");
   need(r >= 1 && r <= n1, "matcomp: need 1 <= r <= n1");
   need(tau_safety >= 1.0, "matcomp: tau_safety must be >= 1");
-  const i64 m = mc_count(n1, n2, r, offset);
+  need(paper_draws >= 0, "matcomp: draws must be >= 0");
+  i64 m = paper_draws > 0 ? 0 : mc_count(n1, n2, r, offset);
   need(m <= n1 * n2, "matcomp: sample count exceeds matrix size");
   Rng rng(seed);
   McData out;
   out.hidden_U = gaussian_matrix(n1, r, rng);
   out.hidden_V = gaussian_matrix(n2, r, rng);
-  // Omega: rejection sampling of distinct (i,j), then sorted by (i,j).
   std::vector<u64> keys;
-  keys.reserve(static_cast<size_t>(m));
-  {
+  if (paper_draws > 0) {
+    keys.resize(static_cast<size_t>(paper_draws));
+    for (auto& key : keys) {
+      const u64 i = rng.uniform_below(u64(n1));
+      const u64 j = rng.uniform_below(u64(n2));
+      key = i * u64(n2) + j;
+    }
+    std::sort(keys.begin(), keys.end());
+    keys.erase(std::unique(keys.begin(), keys.end()), keys.end());
+    m = i64(keys.size());
+  } else {
+    // Omega: rejection sampling of distinct (i,j), then sorted by (i,j).
+    keys.reserve(static_cast<size_t>(m));
     std::unordered_set<u64> seen;
     seen.reserve(static_cast<size_t>(m) * 2);
     while (i64(seen.size()) < m) {
@@ -242,8 +255,8 @@ McData matrix_completion(i64 n1, i64 n2, int r, u64 seed, bool offset,
       const u64 key = i * u64(n2) + j;
       if (seen.insert(key).second) keys.push_back(key);
     }
+    std::sort(keys.begin(), keys.end());  // (i,j) order == key order
   }
-  std::sort(keys.begin(), keys.end());  // (i,j) order == key order
   out.omega_i.resize(static_cast<size_t>(m));
   out.omega_j.resize(static_cast<size_t>(m));
   for (i64 k = 0; k < m; ++k) {

@@ -184,7 +184,7 @@ struct McData {
 };
 i64 mc_count(i64 n1, i64 n2, int r, bool offset);
 McData matrix_completion(i64 n1, i64 n2, int r, u64 seed, bool offset,
-                         double tau_safety);
+                         double tau_safety, i64 paper_draws = 0);
 
 struct PrData {
   Instance inst;

@@ -386,6 +386,9 @@ class McSpec:
     seed: int = 0
     offset_sample_count: bool = False
     tau_safety: float = 1.2
+    # not in the reference: draws_per_dim > 0 selects the paper's sampling rule,
+    # draws_per_dim * (n1 + n2) draws with replacement, deduplicated
+    draws_per_dim: int = 0
 
 
 def matcomp_constraint_count(n1, n2, r, offset_sample_count=False) -> int:
@@ -395,9 +398,15 @@ def matcomp_constraint_count(n1, n2, r, offset_sample_count=False) -> int:
 
 def gen_matrix_completion(spec: McSpec) -> SdpInstance:
     """gen_matrix_completion (instances.cpp:131-234); returns the instance
-    (omega via ``inst.pairs()``, ||M||_* via ``inst.nuclear_norm``)."""
-    return _new(_lib.cuhallar_gen_matrix_completion, C.c_int64(spec.n1), C.c_int64(spec.n2),
-                C.c_int(spec.r), C.c_uint64(spec.seed), C.c_int(int(spec.offset_sample_count)),
+    (omega via ``inst.pairs()``, ||M||_* via ``inst.nuclear_norm``).  With
+    ``spec.draws_per_dim > 0`` the paper's sampling rule replaces the reference's."""
+    if spec.draws_per_dim > 0:
+        return _new(_lib.cuhallar_gen_matrix_completion_paper, C.c_int64(spec.n1), C.c_int64(spec.n2),
+                    C.c_int(spec.r), C.c_uint64(spec.seed),
+                    C.c_int64(spec.draws_per_dim * (spec.n1 + spec.n2)), C.c_double(spec.tau_safety),
+                    kind="matcomp")
+    return _new(_lib.cuhallar_gen_matrix_completion, C.c_int64(spec.n1), C.c_int64(spec.n2), C.c_int(spec.r),
+                C.c_uint64(spec.seed), C.c_int(int(spec.offset_sample_count)),
                 C.c_double(spec.tau_safety), kind="matcomp")
 
 

@@ -803,6 +803,15 @@ int cuhallar_gen_matrix_completion(int64_t n1, int64_t n2, int r, uint64_t seed,
     return 0;
   });
 }
+int cuhallar_gen_matrix_completion_paper(int64_t n1, int64_t n2, int r, uint64_t seed,
+                                         int64_t draws, double tau_safety,
+                                         cuhallar_instance** out) {
+  return guard([&] {
+    if (draws < 1) throw hh::InputError("matcomp: draws must be >= 1");
+    *out = finish_pairs(hh::make_matcomp(n1, n2, r, seed, false, tau_safety, draws));
+    return 0;
+  });
+}
 int64_t cuhallar_matcomp_constraint_count(int64_t n1, int64_t n2, int r, int offset) {
   return hh::matcomp_count(n1, n2, r, offset != 0);
 }

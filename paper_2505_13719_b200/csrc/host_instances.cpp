@@ -331,20 +331,32 @@ double nuclear_small(std::vector<double> A, int r) {
 }  // namespace
 
 HostInst make_matcomp(int64_t n1, int64_t n2, int r, uint64_t seed, bool offset,
-                      double tau_safety) {
+                      double tau_safety, int64_t paper_draws) {
   if (!(n1 >= 1 && n2 >= n1)) throw InputError("matcomp: need n2 >= n1 >= 1");
   if (!(r >= 1 && r <= n1)) throw InputError("matcomp: need 1 <= r <= n1");
   if (!(tau_safety >= 1.0)) throw InputError("matcomp: tau_safety must be >= 1");
   if (n1 + n2 >= (int64_t(1) << 31)) throw InputError("matcomp: n1 + n2 >= 2^31");
-  const int64_t m = matcomp_count(n1, n2, r, offset);
+  if (paper_draws < 0) throw InputError("matcomp: draws must be >= 0");
+  int64_t m = paper_draws > 0 ? 0 : matcomp_count(n1, n2, r, offset);
   if (m > n1 * n2) throw InputError("matcomp: sample count exceeds matrix size");
   Xoshiro g(seed);
   std::vector<double> U(size_t(n1) * r), V(size_t(n2) * r);  // column-major fills
   for (auto& x : U) x = g.normal();
   for (auto& x : V) x = g.normal();
   std::vector<uint64_t> keys;
-  keys.reserve(size_t(m));
-  {
+  if (paper_draws > 0) {
+    // the paper's rule: draws with replacement, deduplicated
+    keys.resize(size_t(paper_draws));
+    for (auto& key : keys) {
+      const uint64_t i = g.below(uint64_t(n1));
+      const uint64_t j = g.below(uint64_t(n2));
+      key = i * uint64_t(n2) + j;
+    }
+    radix_sort(keys);
+    keys.erase(std::unique(keys.begin(), keys.end()), keys.end());
+    m = int64_t(keys.size());
+  } else {
+    keys.reserve(size_t(m));
     KeySet set(uint64_t(m) + 1);
     while (int64_t(keys.size()) < m) {
       const uint64_t i = g.below(uint64_t(n1));
@@ -352,8 +364,8 @@ HostInst make_matcomp(int64_t n1, int64_t n2, int r, uint64_t seed, bool offset,
       const uint64_t key = i * uint64_t(n2) + j;
       if (set.insert(key)) keys.push_back(key);
     }
+    radix_sort(keys);  // (i, j) lexicographic == key order
   }
-  radix_sort(keys);  // (i, j) lexicographic == key order
   HostInst h;
   h.family = 1;
   h.n = n1 + n2;

@@ -65,8 +65,10 @@ Edges normalise_edges(int64_t n_hint, const Edges& raw, int64_t* n_out);
 
 HostInst make_theta(int64_t n, const Edges& sorted_unique_edges);
 int64_t matcomp_count(int64_t n1, int64_t n2, int r, bool offset);
+// paper_draws > 0: the paper's sampling rule (that many draws with replacement,
+// deduplicated) instead of instances.cpp:123-159
 HostInst make_matcomp(int64_t n1, int64_t n2, int r, uint64_t seed, bool offset,
-                      double tau_safety);
+                      double tau_safety, int64_t paper_draws = 0);
 HostInst make_phaseret(int64_t n, int L, uint64_t seed, double tau_slack);
 
 // Eigen LinearVectorized redux order (SSE2, 2 accumulators of 2 lanes).

@@ -1,6 +1,7 @@
 """Time-to-1e-5 on the large north-star instances (one device solve each).
 
-python scripts/solve_large.py H20 H23 mc400000_600000_3 --time-limit 600 [--profile]
+python scripts/solve_large.py H20 H23 mc400000_600000_3 mcp3200000_4800000_3 --time-limit 600 [--profile]
+(mcpN1_N2_R: the paper's sampling rule, 40 (n1 + n2) draws with replacement, deduplicated)
 Prints one JSON line per instance: generation time, device seconds, counters,
 residuals, and (with --profile) the per-phase device-time breakdown.
 """
@@ -17,6 +18,9 @@ sys.path.insert(0, ROOT)
 def build(H, name):
     if name.startswith("H"):
         return H.build_theta_instance(H.make_hypercube(int(name[1:])))
+    if name.startswith("mcp"):  # the paper's sampling rule: 40 (n1 + n2) draws, deduplicated
+        n1, n2, r = [int(x) for x in name[3:].split("_")]
+        return H.gen_matrix_completion(H.McSpec(n1, n2, r, seed=0, draws_per_dim=40))
     if name.startswith("mc"):
         n1, n2, r = [int(x) for x in name[2:].split("_")]
         return H.gen_matrix_completion(H.McSpec(n1, n2, r, seed=0))

@@ -179,3 +179,21 @@ def test_trace_events(H, orc):
     assert len(outer) == rep.outer_iters and all(e.theta >= 0 for e in outer)
     ref = []
     orc.OracleInstance.cycle(5).solve(trace=True)
+
+
+def test_matcomp_paper_rule_instance_and_solve(H, orc):
+    # paper sampling rule: device instance identical to the oracle's
+    inst = H.gen_matrix_completion(H.McSpec(300, 700, 3, seed=1, draws_per_dim=40))
+    ref = orc.OracleInstance.matcomp_paper(300, 700, 3, seed=1, draws_per_dim=40)
+    assert (inst.n, inst.m) == (ref.n, ref.m)
+    i, j = inst.pairs()
+    ri, rj = ref.pairs()
+    assert np.array_equal(i, ri) and np.array_equal(j, rj)
+    assert np.array_equal(inst.b, ref.b)
+    assert inst.tau == pytest.approx(ref.tau, rel=1e-13)
+    small = H.gen_matrix_completion(H.McSpec(30, 70, 2, seed=5, draws_per_dim=12))
+    small_ref = orc.OracleInstance.matcomp_paper(30, 70, 2, seed=5, draws_per_dim=12)
+    rep = H.solve(small)
+    want = small_ref.solve()
+    assert rep.status == "optimal"
+    assert abs(rep.pval - want.pval) <= 1e-6 * abs(want.pval)

@@ -282,3 +282,25 @@ def test_thread_count_invariance(orc):
     orc.lib().orc_set_threads(0)
     for x, y in zip(a, b):
         assert np.array_equal(x, y)
+
+
+def test_matcomp_paper_sampling_rule(orc):
+    # SURVEY §0 item 2 / §8(f) row 2 (not in the reference; parity unpinned against it):
+    # draws_per_dim * (n1 + n2) draws with replacement, deduplicated and sorted
+    n1, n2, d = 300, 700, 40
+    inst = orc.OracleInstance.matcomp_paper(n1, n2, 3, seed=1, draws_per_dim=d)
+    i, j = inst.pairs()
+    draws, N = d * (n1 + n2), n1 * n2
+    assert inst.m == len(i) <= draws
+    keys = i * n2 + j
+    assert np.all(np.diff(keys) > 0)  # sorted, distinct
+    expect = N * (1.0 - (1.0 - 1.0 / N) ** draws)  # expected distinct count
+    assert abs(inst.m - expect) <= 6 * np.sqrt(expect * np.exp(-draws / N))
+    # the paper's 3.2M x 4.8M row: 319,996,871 reported vs this expectation
+    N8, D8 = 3_200_000 * 4_800_000, 40 * 8_000_000
+    assert abs(N8 * (1.0 - np.exp(-D8 / N8)) - 319_996_871) / 319_996_871 < 1e-5
+    # a recoverable small instance solves to ||M||_*
+    small = orc.OracleInstance.matcomp_paper(30, 70, 2, seed=5, draws_per_dim=12)
+    r = small.solve()
+    assert r.status == "optimal"
+    assert abs(r.pval - small.nuclear_norm) / small.nuclear_norm <= 1e-3

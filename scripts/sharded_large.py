@@ -11,6 +11,9 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 def build(H, name):
     if name.startswith("H"):
         return H.build_theta_instance(H.make_hypercube(int(name[1:])))
+    if name.startswith("mcp"):  # the paper's sampling rule
+        n1, n2, r = [int(x) for x in name[3:].split("_")]
+        return H.gen_matrix_completion(H.McSpec(n1, n2, r, seed=0, draws_per_dim=40))
     n1, n2, r = [int(x) for x in name[2:].split("_")]
     return H.gen_matrix_completion(H.McSpec(n1, n2, r, seed=0))
 

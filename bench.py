@@ -255,7 +255,7 @@ def main():
     edges = None
     ei, ej = inst.pairs()
     e2e_times, h2d, d2h = [], 0, 0
-    for k in range(args.steps):
+    for k in range(-1, args.steps):  # one untimed warm-up pass (first-use allocations)
         flush.fill_(float(k))
         torch.cuda.synchronize()
         t0 = time.perf_counter()
@@ -264,7 +264,8 @@ def main():
         r2 = H.solve(inst2, cfg, fetch=True)
         t1 = time.perf_counter()
         assert r2.status == "optimal"
-        e2e_times.append(t1 - t0)
+        if k >= 0:
+            e2e_times.append(t1 - t0)
         h2d = inst2.info()["h2d_bytes"]
         d2h = r2.U.nbytes + r2.p.nbytes
         del inst2

@@ -363,15 +363,36 @@ __device__ __forceinline__ void row_pass_rt(Ctx& c, const Params& P, const UA& U
       const double* __restrict__ pp = upper ? Pup : Plo;
       const double* __restrict__ bp = upper ? I.b_up : I.b_lo;
 #pragma unroll 1
-      for (int64_t e = e0; e < e1; e += B) {
+      for (int64_t e = e0, step = B; e < e1; e += step) {
         int64_t bc[B];
         double pk[B], bk[B];
+        // matrix completion (long rows, three streams per entry): an odd start is
+        // peeled as a one-entry batch so full batches load their column indices,
+        // multipliers and right-hand sides as 8/16-byte pairs (fewer load
+        // instructions: these passes are load-queue throttled); order unchanged
+        step = (has_b && (e & 1)) ? 1 : B;
+        const int lim = (int)min((int64_t)step, e1 - e);
+        if (has_b && lim == B) {
 #pragma unroll
-        for (int u = 0; u < B; ++u) {
-          const bool ok = e + u < e1;
-          bc[u] = ok ? (int64_t)__ldg(colp + e + u) : a;
-          pk[u] = ok ? __ldg(pp + e + u) : 0.0;
-          bk[u] = (ok && has_b) ? __ldg(bp + e + u) : 0.0;
+          for (int u = 0; u < B; u += 2) {
+            const int2 cv = __ldg(reinterpret_cast<const int2*>(colp + e + u));
+            const double2 pv = __ldg(reinterpret_cast<const double2*>(pp + e + u));
+            const double2 bv = __ldg(reinterpret_cast<const double2*>(bp + e + u));
+            bc[u] = cv.x;
+            bc[u + 1] = cv.y;
+            pk[u] = pv.x;
+            pk[u + 1] = pv.y;
+            bk[u] = bv.x;
+            bk[u + 1] = bv.y;
+          }
+        } else {
+#pragma unroll
+          for (int u = 0; u < B; ++u) {
+            const bool ok = u < lim;
+            bc[u] = ok ? (int64_t)__ldg(colp + e + u) : a;
+            pk[u] = ok ? __ldg(pp + e + u) : 0.0;
+            bk[u] = (ok && has_b) ? __ldg(bp + e + u) : 0.0;
+          }
         }
         double ub[B][S];
 #pragma unroll
@@ -380,7 +401,7 @@ __device__ __forceinline__ void row_pass_rt(Ctx& c, const Params& P, const UA& U
           for (int k = 0; k < S; ++k) ub[u][k] = U(bc[u] * S + k);
 #pragma unroll
         for (int u = 0; u < B; ++u) {
-          if (e + u >= e1) break;
+          if (u >= lim) break;
           double w;
           if (FIXED) {
             w = 0.5 * pk[u];

@@ -149,6 +149,9 @@ typedef struct {
   int trace;     /* deliver TraceEvents to the callback (costs one extra map per rank step) */
   int team_ctas; /* 0 = one persistent CTA per SM slot (auto) */
   int profile;   /* record per-phase device time (cuhallar_last_profile) */
+  int parity;    /* 1 = parity mode: every reduction in the reference binary's order
+                    (Eigen LinearVectorized redux, ordered CGS2 dots),
+                    so counters match the CPU oracle; pair families, one GPU, slower */
 } cuhallar_config;
 /* Fills the reference defaults. */
 void cuhallar_config_default(cuhallar_config* cfg);
@@ -211,6 +214,12 @@ int cuhallar_min_eig_gradient(cuhallar_instance* inst, const double* U_host, int
                               const double* p_host, double beta, double tol, int max_iters,
                               int block_restart, uint64_t seed, double* lambda,
                               double* v_host, double* residual, int* matvecs, int* converged);
+/* As cuhallar_min_eig_gradient with EigSettings taken from cfg (eig_max_iters,
+ * eig_block_restart, seed) and cfg->parity selecting the checker-order mode. */
+int cuhallar_min_eig_gradient_cfg(cuhallar_instance* inst, const double* U_host, int s,
+                                  const double* p_host, double beta, double tol,
+                                  const cuhallar_config* cfg, double* lambda, double* v_host,
+                                  double* residual, int* matvecs, int* converged);
 /* aipp_run on g = L_beta(.;p) from W_host (adap_aipp.cpp:40-116) */
 int cuhallar_aipp(cuhallar_instance* inst, const double* p_host, double beta,
                   const double* W_host, int s, double rho, const cuhallar_config* cfg,
@@ -226,6 +235,10 @@ int cuhallar_aipp(cuhallar_instance* inst, const double* p_host, double beta,
 int cuhallar_bench_pass(cuhallar_instance* inst, int kind, const double* U_host, int s,
                         const double* p_host, double beta, int iters, int team_ctas,
                         double* ns_per_pass);
+
+/* The trace ring of the last traced launch (events in order, also the debug
+ * kinds 9 = fista() call and 10 = parity job-phase results); returns the count. */
+int cuhallar_last_trace(const cuhallar_instance* inst, cuhallar_trace_event* out, int cap);
 
 /* Per-phase device time of the last profiled solve (cfg.profile = 1):
  * categories 0 fista_x~, 1 fista_value_grad, 2 fista_y+_map, 3 fista_grad_y+,

@@ -4,6 +4,8 @@
 // hlr.cpp and solver.cpp statement by statement (cited per function).
 // TEST INFRASTRUCTURE ONLY (see orc.hpp).
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <limits>
 
 #include "orc.hpp"
@@ -41,6 +43,19 @@ double sqdist(const Mat& a, const Mat& b) {
   });
 }
 }  // namespace
+
+// Debug record of every fista() call (ORC_DEBUG_FISTA=<file>): used to locate
+// the first divergence between the parity-mode device solve and this checker.
+static void dbg_fista(double L0, int status, int iters, double L, double psi_y, int cap) {
+  static FILE* f = [] {
+    const char* p = std::getenv("ORC_DEBUG_FISTA");
+    return p ? std::fopen(p, "w") : nullptr;
+  }();
+  if (f) {
+    std::fprintf(f, "%.17g %d %d %.17g %.17g %d\n", L0, status, iters, L, psi_y, cap);
+    std::fflush(f);
+  }
+}
 
 // ------------------------------------------------------------- AL core ---
 // sdp_instance.cpp:50-60
@@ -138,6 +153,7 @@ FistaResult fista(const Smooth& psi, const Mat& x0, const FistaParams& prm) {
       out.v = Mat(x0.rows, x0.cols);
       out.L = L;
       out.iters = it;
+      dbg_fista(prm.L0, 2, it, L, 0.0, cap);
       return out;
     }
     double a = 0, psi_t = 0, psi_n = 0, dsq = 0;
@@ -178,6 +194,7 @@ FistaResult fista(const Smooth& psi, const Mat& x0, const FistaParams& prm) {
       out.iters = it + 1;
       out.x_tilde = xt;
       out.A = A_next;
+      dbg_fista(prm.L0, 1, it + 1, L, psi_n, -1);
       return out;
     }
     const Mat gy = psi.gradient(yn);
@@ -193,6 +210,7 @@ FistaResult fista(const Smooth& psi, const Mat& x0, const FistaParams& prm) {
       out.iters = it + 1;
       out.x_tilde = xt;
       out.A = A_next;
+      dbg_fista(prm.L0, 0, it + 1, L, psi_n, -1);
       return out;
     }
     A = A_next;

@@ -79,6 +79,7 @@ class CConfig(C.Structure):
         ("fista_chi", C.c_double), ("fista_mu", C.c_double), ("fista_L0", C.c_double),
         ("fista_max_iters", C.c_int), ("max_fw_steps", C.c_int), ("threads", C.c_int),
         ("trace", C.c_int), ("team_ctas", C.c_int), ("profile", C.c_int),
+        ("parity", C.c_int),
     ]
 
 
@@ -115,7 +116,8 @@ class CTrace(C.Structure):
 _TRACE_FN = C.CFUNCTYPE(None, C.POINTER(CTrace), C.c_void_p)
 
 STATUS = {0: "optimal", 1: "iteration_limit", 2: "time_limit", 3: "numerical_failure"}
-TRACE_KIND = {0: "inner_stationary", 1: "inner_rank_step", 2: "outer"}
+TRACE_KIND = {0: "inner_stationary", 1: "inner_rank_step", 2: "outer", 9: "fista_debug",
+              10: "parity_jobs"}
 
 
 def version() -> str:
@@ -303,17 +305,27 @@ class SdpInstance:
         return v.value, out.t().cpu().numpy()
 
     # -- sub-solvers (parity testing) --
-    def min_eig_gradient(self, U, p, beta, tol=1e-8, max_iters=5000, block_restart=30, seed=0):
+    def min_eig_gradient(self, U, p, beta, tol=1e-8, max_iters=5000, block_restart=30, seed=0,
+                         parity=False):
         U = np.asfortranarray(np.asarray(U, dtype=np.float64).reshape(self.n, -1))
         p = np.ascontiguousarray(p, dtype=np.float64)
         lam, res = C.c_double(), C.c_double()
         mv, conv = C.c_int(), C.c_int()
         v = np.empty(self.n)
-        _check(_lib.cuhallar_min_eig_gradient(
+        cc = SolverConfig(eig_max_iters=max_iters, eig_block_restart=block_restart, seed=seed,
+                          parity=parity)._c()
+        _check(_lib.cuhallar_min_eig_gradient_cfg(
             self._h, U.ctypes.data_as(_dp), C.c_int(U.shape[1]), p.ctypes.data_as(_dp), C.c_double(beta),
-            C.c_double(tol), C.c_int(max_iters), C.c_int(block_restart), C.c_uint64(seed), C.byref(lam),
+            C.c_double(tol), C.byref(cc), C.byref(lam),
             v.ctypes.data_as(_dp), C.byref(res), C.byref(mv), C.byref(conv)))
         return dict(lambda_=lam.value, v=v, residual=res.value, matvecs=mv.value, converged=bool(conv.value))
+
+    def last_trace(self, cap=1 << 16) -> list:
+        """Raw events of the last traced launch (tuples: kind, outer_iter, beta, eps_inner, gap,
+        theta, rank, al_value, fw_alpha, rel_pfeas, rel_gap, rel_dfeas)."""
+        buf = (CTrace * cap)()
+        k = _lib.cuhallar_last_trace(self._h, buf, cap)
+        return [tuple(getattr(buf[i], f) for f, _ in CTrace._fields_) for i in range(k)]
 
     PROFILE_CATS = ["fista_x~", "fista_value_grad", "fista_y+_map", "fista_grad_y+", "aipp",
                     "lanczos_apply", "lanczos_cgs2", "jacobi", "lanczos_measure", "lanczos_restart",
@@ -454,14 +466,23 @@ class SolverConfig:
     threads: int = 0
     team_ctas: int = 0
     profile: bool = False
+    # parity mode: every reduction in the reference binary's order so the
+    # iteration counters match the CPU oracle (pair families, one GPU, slower)
+    parity: bool = False
 
     def _c(self, trace=False) -> CConfig:
         c = CConfig()
         for name, _ in CConfig._fields_:
             if name == "trace":
-                c.trace = 1 if trace else 0
+                # debug (parity mode): CUHALLAR_DEBUG_FISTA=1 adds one "fista_debug" event per
+                # FISTA call; CUHALLAR_DEBUG_JOBS=1 also records every job phase (inst.last_trace())
+                c.trace = (2 if os.environ.get("CUHALLAR_DEBUG_FISTA") else 1) if trace else 0
+                if os.environ.get("CUHALLAR_DEBUG_JOBS"):
+                    c.trace = 3
             elif name == "profile":
                 c.profile = 1 if self.profile else 0
+            elif name == "parity":
+                c.parity = 1 if self.parity else 0
             else:
                 setattr(c, name, getattr(self, name))
         return c

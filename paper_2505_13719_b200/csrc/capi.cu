@@ -14,6 +14,7 @@
 
 #include "../../include/cuhallar.h"
 #include "host_instances.hpp"
+#include "kernel_setup.cuh"
 #include "solve.cuh"
 
 using namespace hallar;
@@ -25,109 +26,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     hallar_kernel(const __grid_constant__ Params P, SolveOut* so) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Ctx c;
-  c.t.rank = P.fab.me * gridDim.x + blockIdx.x;  // global CTA index over all ranks
-  c.t.size = P.fab.world * gridDim.x;
-  c.t.lrank = blockIdx.x;
-  c.t.lsize = gridDim.x;
-  c.t.fab = &P.fab;
-  c.t.mw = P.fab.world > 1;
-  c.t.bar = P.bar;
-  c.t.slots = P.slots;
-  c.t.epoch = 0;
-  c.t.parity = 0;
-  c.warp = threadIdx.x >> 5;
-  c.lane = threadIdx.x & 31;
-  double* sm = reinterpret_cast<double*>(smem_raw);
-  c.rs.part = sm;
-  sm += kWarps * kRedK;
-  c.rs.out = sm;
-  sm += kRedK;
-  {
-    // one pass scratch: tile-engine arrays, or the phase-retrieval transform
-    double* base = sm;
-    c.X = reinterpret_cast<double2*>(base);
-    c.tw = sm;
-    sm += kGroups * kTileEntries;
-    c.tterm = sm;
-    sm += kGroups * 4 * kTileEntries;
-    c.vlo = reinterpret_cast<int64_t*>(sm);
-    sm += 2 * kGroups * (kTileRows + 1);
-    c.vup = reinterpret_cast<int64_t*>(sm);
-    sm += 2 * kGroups * (kTileRows + 1);
-    c.tcol = reinterpret_cast<int32_t*>(sm);
-    sm = base + P.pass_scratch;  // tile arrays (pairs) or one transform (phase retrieval)
-  }
-  c.cs = sm;
-  sm += 2 * kSMax;
-  c.H = sm;
-  sm += kHLd * kHLd;
-  c.JA = sm;
-  sm += 32 * 32;
-  c.JV = sm;
-  sm += 32 * 32;
-  c.E = sm;
-  sm += 32 * 32;
-  c.ev = sm;
-  sm += 32;
-  c.jcs = sm;
-  sm += 32;
-  c.hh = sm;
-  sm += 32;
-  c.hh2 = sm;
-  sm += 32;
-  c.vsum = sm;
-  sm += 64;
-  int* ip = reinterpret_cast<int*>(sm);
-  c.col = ip;
-  ip += 40;
-  c.jpq = ip;
-  ip += 40;
-  c.ccol = ip;
-  ip += kCacheEnt;
-  c.crlo = ip;
-  ip += kCacheRows + 1;
-  c.crup = ip;
-  ip += kCacheRows + 1;
-  c.ctr = ip;
-  if (P.I.family == kPhaseret) {
-    c.tl = c.th = 0;
-    c.rl = P.I.n * c.t.rank / c.t.size;
-    c.rh = P.I.n * (c.t.rank + 1) / c.t.size;
-  } else {
-    c.tl = P.I.ntiles * c.t.rank / c.t.size;
-    c.th = P.I.ntiles * (c.t.rank + 1) / c.t.size;
-    c.rl = P.I.tile_row[c.tl];
-    c.rh = P.I.tile_row[c.th];
-  }
-  if (P.I.family != kPhaseret) {
-    // static structure of the CTA's rows -> shared memory (small instances)
-    const int64_t lo0 = P.I.lo_ptr[c.rl], up0 = P.I.up_ptr[c.rl];
-    const int64_t nlo = P.I.lo_ptr[c.rh] - lo0, nup = P.I.up_ptr[c.rh] - up0;
-    c.cached = c.th - c.tl <= kCacheTiles && c.rh - c.rl <= kCacheRows &&
-               nlo + nup <= kCacheEnt;
-    if (c.cached) {
-      c.clo0 = lo0;
-      c.cup0 = up0;
-      c.cnlo = (int32_t)nlo;
-      for (int64_t r = threadIdx.x; r <= c.rh - c.rl; r += kThreads) {
-        c.crlo[r] = (int32_t)(P.I.lo_ptr[c.rl + r] - lo0);
-        c.crup[r] = (int32_t)(P.I.up_ptr[c.rl + r] - up0);
-      }
-      for (int64_t t = threadIdx.x; t <= c.th - c.tl; t += kThreads)
-        c.ctr[t] = (int32_t)(P.I.tile_row[c.tl + t] - c.rl);
-      for (int64_t e = threadIdx.x; e < nlo; e += kThreads) c.ccol[e] = P.I.lo_col[lo0 + e];
-      for (int64_t e = threadIdx.x; e < nup; e += kThreads) c.ccol[nlo + e] = P.I.ej[up0 + e];
-    }
-    __syncthreads();
-  }
-  if (P.fab.world > 1) {
-    // row-owner sharding: a CTA owns the upper (edge-order) entries of its rows
-    c.kl = P.I.up_ptr[c.rl];
-    c.kh = P.I.up_ptr[c.rh];
-  } else {
-    c.kl = P.I.np * c.t.rank / c.t.size;
-    c.kh = P.I.np * (c.t.rank + 1) / c.t.size;
-  }
+  setup_ctx(c, P, smem_raw);
   if (P.op == kOpSolve) {
     solve_dev(c, P, so);
   } else {
@@ -158,17 +57,16 @@ __global__ void gather_lower(const double* __restrict__ src, const int64_t* __re
 }
 }  // namespace hallar
 
+namespace hallar {
+// parity_kernel.cu
+const void* hallar_parity_kernel_fn();
+int hallar_parity_prepare();  // sets the smem attribute; returns resident CTAs per SM
+}  // namespace hallar
+
 namespace {
 
 thread_local std::string g_err;
 
-// dynamic shared memory: fixed solver state + the pass scratch of the family
-constexpr size_t smem_bytes(int pass_scratch) {
-  return sizeof(double) * (kWarps * kRedK + kRedK + pass_scratch + 2 * kSMax + kHLd * kHLd +
-                           3 * 32 * 32 + 4 * 32 + 64) +
-         sizeof(int) * (80 + kCacheInts);
-}
-constexpr size_t kSmemBytes = smem_bytes(kPassScratch);  // the largest (attribute, occupancy)
 
 struct CudaError : std::runtime_error {
   using std::runtime_error::runtime_error;
@@ -213,6 +111,9 @@ int grid_size(int requested) {
     ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, hallar_kernel, kThreads, kSmemBytes),
        "occupancy");
     if (per < 1) throw CudaError("hallar_kernel cannot be resident");
+    const int pp = hallar_parity_prepare();  // same team size for both persistent kernels
+    if (pp < 1) throw CudaError("hallar_parity_kernel cannot be resident");
+    per = std::min(per, pp);
     cached = std::min(sms * per, kMaxTeam);
   }
   if (requested > 0) return std::min(requested, cached);
@@ -261,7 +162,7 @@ struct cuhallar_instance {
   std::vector<unsigned long long> last_prof;
   TraceEv* trace_host = nullptr;
   int* trace_count_host = nullptr;
-  int trace_cap = 4096;
+  int trace_cap = 65536;
   std::mutex mu;
 
   ~cuhallar_instance() {
@@ -517,6 +418,7 @@ Cfg to_dev_cfg(const cuhallar_config& c) {
   d.fista_max_iters = c.fista_max_iters;
   d.max_fw_steps = c.max_fw_steps;
   d.trace = c.trace;
+  d.parity = c.parity;
   return d;
 }
 
@@ -627,8 +529,10 @@ int launch(cuhallar_instance* in, Params& P, int grid, cudaStream_t st, SolveOut
     ck(cudaEventCreate(&e1), "event");
     ck(cudaEventRecord(e0, st), "event");
   }
-  ck(cudaLaunchCooperativeKernel((void*)hallar_kernel, dim3(grid), dim3(kThreads), args,
-                                 smem_bytes(P.pass_scratch), st),
+  // parity mode (parity.cuh) runs in its own persistent kernel (parity_kernel.cu)
+  const bool par = P.cfg.parity && (P.op == kOpSolve || P.op == kOpMinEigG || P.op == kOpAipp);
+  ck(cudaLaunchCooperativeKernel(par ? hallar_parity_kernel_fn() : (const void*)hallar_kernel,
+                                 dim3(grid), dim3(kThreads), args, smem_bytes(P.pass_scratch), st),
      "cooperative launch");
   if (ms) ck(cudaEventRecord(e1, st), "event");
   ck(cudaMemcpyAsync(so, in->dso, sizeof(SolveOut), cudaMemcpyDeviceToHost, st), "D2H out");
@@ -997,6 +901,8 @@ int cuhallar_solve(cuhallar_instance* in, const cuhallar_config* cfg, const doub
   return guard([&] {
     DevGuard dg(in->device);
     validate_cfg(*cfg);
+    if (cfg->parity && in->h.family == kPhaseret)
+      throw hh::InputError("parity mode: pair families only (theta, matrix completion)");
     std::lock_guard<std::mutex> lk(in->mu);
     const auto t_start = std::chrono::steady_clock::now();
     const int64_t n = in->h.n;
@@ -1118,6 +1024,7 @@ int cuhallar_solve_sharded(cuhallar_instance* const* insts, int world, const cuh
   return guard([&] {
     if (world < 1 || world > kMaxWorld) throw hh::InputError("sharded solve: world must lie in [1, 8]");
     validate_cfg(*cfg);
+    if (cfg->parity) throw hh::InputError("parity mode: single-GPU solve only");
     std::vector<cuhallar_instance*> R(insts, insts + world);
     for (int r = 0; r < world; ++r) {
       if (!R[r]) throw hh::InputError("sharded solve: null instance");
@@ -1243,6 +1150,18 @@ int cuhallar_solve_sharded(cuhallar_instance* const* insts, int world, const cuh
   });
 }
 
+int cuhallar_last_trace(const cuhallar_instance* in, cuhallar_trace_event* out, int cap) {
+  if (!in->trace_host || !in->trace_count_host) return 0;
+  const int cnt = std::min(std::min(*in->trace_count_host, in->trace_cap), cap);
+  for (int i = 0; i < cnt; ++i) {
+    const TraceEv& e = in->trace_host[i];
+    out[i] = cuhallar_trace_event{e.kind, e.outer_iter, e.beta, e.eps_inner, e.gap, e.theta,
+                                  e.rank, e.al_value, e.fw_alpha, e.rel_pfeas, e.rel_gap,
+                                  e.rel_dfeas};
+  }
+  return cnt;
+}
+
 int cuhallar_last_profile(const cuhallar_instance* in, double* ns, int64_t* counts, int cap) {
   if (in->last_prof.empty()) return 0;
   const int k = std::min<int>(cap, kProfCats);
@@ -1263,11 +1182,13 @@ int cuhallar_solution_get_p(const cuhallar_solution* s, double* p) {
 }
 void cuhallar_solution_destroy(cuhallar_solution* s) { delete s; }
 
-int cuhallar_min_eig_gradient(cuhallar_instance* in, const double* U_host, int s,
-                              const double* p_host, double beta, double tol, int max_iters,
-                              int block_restart, uint64_t seed, double* lambda, double* v_host,
-                              double* residual, int* matvecs, int* converged) {
+static int min_eig_impl(cuhallar_instance* in, const double* U_host, int s, const double* p_host,
+                        double beta, double tol, int max_iters, int block_restart, uint64_t seed,
+                        int parity, double* lambda, double* v_host, double* residual,
+                        int* matvecs, int* converged) {
   return guard([&] {
+    if (parity && in->h.family == kPhaseret)
+      throw hh::InputError("parity mode: pair families only (theta, matrix completion)");
     DevGuard dg(in->device);
     if (s < 1 || s > kSMax) throw hh::InputError("factor rank must be in [1, 32]");
     if (block_restart < 2 || block_restart > kLanczosMax)
@@ -1279,6 +1200,7 @@ int cuhallar_min_eig_gradient(cuhallar_instance* in, const double* U_host, int s
     cuhallar_config_default(&cfg);
     cfg.eig_max_iters = max_iters;
     cfg.eig_block_restart = block_restart;
+    cfg.parity = parity;
     Params P = base_params(in, &cfg);
     P.op = kOpMinEigG;
     use_unscaled_b(in, P);
@@ -1305,6 +1227,22 @@ int cuhallar_min_eig_gradient(cuhallar_instance* in, const double* U_host, int s
   });
 }
 
+int cuhallar_min_eig_gradient(cuhallar_instance* in, const double* U_host, int s,
+                              const double* p_host, double beta, double tol, int max_iters,
+                              int block_restart, uint64_t seed, double* lambda, double* v_host,
+                              double* residual, int* matvecs, int* converged) {
+  return min_eig_impl(in, U_host, s, p_host, beta, tol, max_iters, block_restart, seed, 0, lambda,
+                      v_host, residual, matvecs, converged);
+}
+
+int cuhallar_min_eig_gradient_cfg(cuhallar_instance* in, const double* U_host, int s,
+                                  const double* p_host, double beta, double tol,
+                                  const cuhallar_config* cfg, double* lambda, double* v_host,
+                                  double* residual, int* matvecs, int* converged) {
+  return min_eig_impl(in, U_host, s, p_host, beta, tol, cfg->eig_max_iters, cfg->eig_block_restart,
+                      cfg->seed, cfg->parity, lambda, v_host, residual, matvecs, converged);
+}
+
 int cuhallar_aipp(cuhallar_instance* in, const double* p_host, double beta, const double* W_host,
                   int s, double rho, const cuhallar_config* cfg, double* W_out, int* status,
                   int* prox_iters, int* fista_iters, double* R_norm, double* g_value,
@@ -1312,9 +1250,16 @@ int cuhallar_aipp(cuhallar_instance* in, const double* p_host, double beta, cons
   return guard([&] {
     DevGuard dg(in->device);
     if (s < 1 || s > kSMax) throw hh::InputError("factor rank must be in [1, 32]");
+    if (cfg && cfg->parity && in->h.family == kPhaseret)
+      throw hh::InputError("parity mode: pair families only (theta, matrix completion)");
     std::lock_guard<std::mutex> lk(in->mu);
     const int grid = grid_size(cfg ? cfg->team_ctas : 0);
     ensure_workspace(in, grid, 0, 30);
+    if (cfg && cfg->trace && !in->trace_host) {
+      ck(cudaHostAlloc(&in->trace_host, sizeof(TraceEv) * in->trace_cap, cudaHostAllocMapped),
+         "trace ring");
+      ck(cudaHostAlloc(&in->trace_count_host, sizeof(int), cudaHostAllocMapped), "trace count");
+    }
     Params P = base_params(in, cfg);
     P.op = kOpAipp;
     use_unscaled_b(in, P);

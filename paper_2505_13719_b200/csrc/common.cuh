@@ -109,6 +109,7 @@ struct Cfg {
   double fista_sigma, fista_chi, fista_mu, fista_L0;
   int fista_max_iters, max_fw_steps;
   int trace;
+  int parity;  // reductions in the checker's order (parity.cuh)
 };
 
 struct TraceEv {

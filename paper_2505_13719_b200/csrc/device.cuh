@@ -72,6 +72,7 @@ struct Ctx {
   int status = kOk;
   int msg = kMsgNone;
   unsigned long long prof_last = 0;
+  const Params* Pp = nullptr;  // launch parameters (debug hooks)
   double beta = 0.0;     // current AL penalty (replicated)
   double p_trace = 0.0;  // current p[m-1] (theta trace multiplier)
 };
@@ -101,10 +102,10 @@ __device__ __forceinline__ void fail(Ctx& c, int status, int msg) {
 
 // ------------------------------------------------------------------ layout --
 // Rows are split so that (lower + upper entries + 8) is balanced per CTA.
-__device__ int64_t work_prefix(const DevPairs& I, int64_t a) {
+inline __device__ int64_t work_prefix(const DevPairs& I, int64_t a) {
   return I.lo_ptr[a] + I.up_ptr[a] + 8 * a;
 }
-__device__ int64_t row_split(const DevPairs& I, int rank, int size) {
+inline __device__ int64_t row_split(const DevPairs& I, int rank, int size) {
   if (rank <= 0) return 0;
   if (rank >= size) return I.n;
   const int64_t total = work_prefix(I, I.n);
@@ -794,7 +795,7 @@ __device__ __forceinline__ void gradop_pass(Ctx& c, const Params& P, const doubl
 // Thread per pair constraint k (edge order): d_k = U_{i_k}.U_{j_k} summed over
 // columns in order (instances.cpp:27-35).  kUnroll constraints per thread are
 // loaded before any is used so each thread keeps several gathers in flight.
-enum MapMode : int { kMapPR = 0, kMapRR = 1, kMapOut = 2, kMapFWS = 3 };
+enum MapMode : int { kMapPR = 0, kMapRR = 1, kMapOut = 2, kMapFWS = 3, kMapROut = 4 };
 constexpr int kUnroll = 4;
 
 // Row values of the gathered factor: either stored (U) or produced on the fly
@@ -856,6 +857,8 @@ __device__ __forceinline__ void map_pass_src(Ctx& c, const Params& P, const RowS
       if (k >= c.kh) continue;
       if (mode == kMapOut) {
         out[k] = d[u];
+      } else if (mode == kMapROut) {
+        out[k] = d[u] - bk[u];  // residual_of (algo: r[k] = map[k] - b[k])
       } else if (mode == kMapFWS) {
         const double t = (rf[u] + bk[u]) - d[u];
         sums[1] = sums[1] + t * t;

@@ -98,7 +98,7 @@ __device__ __noinline__ bool certify_dev(Ctx& c, const Params& P, const double* 
 
 // solve (solver.cpp:136-279) from buffers[0] (rank P.s_in) and the
 // multiplier already loaded into p_up / p_lo / P.p_trace.
-__device__ __noinline__ void solve_dev(Ctx& c, const Params& P, SolveOut* so) {
+inline __device__ __noinline__ void solve_dev(Ctx& c, const Params& P, SolveOut* so) {
   const DevPairs& I = P.I;
   const Cfg& cf = P.cfg;
   const double t0 = team_now(c);

@@ -23,13 +23,13 @@ __device__ __forceinline__ unsigned long long globaltimer_ns() {
 }
 
 // Team-consistent clock: CTA 0's timer, broadcast through a reduction.
-__device__ __noinline__ double team_now(Ctx& c) {
+inline __device__ __noinline__ double team_now(Ctx& c) {
   double v[1] = {(c.t.rank == 0 && threadIdx.x == 0) ? (double)globaltimer_ns() : 0.0};
   team_sum<1>(c.t, c.rs, v);
   return v[0];
 }
 
-__device__ void emit_trace(const Params& P, Ctx& c, const TraceEv& ev) {
+inline __device__ void emit_trace(const Params& P, Ctx& c, const TraceEv& ev) {
   if (!P.cfg.trace || c.t.rank != 0 || threadIdx.x != 0 || !P.trace) return;
   const int i = *P.trace_count;
   if (i < P.trace_cap) P.trace[i] = ev;
@@ -45,7 +45,7 @@ __device__ void emit_trace(const Params& P, Ctx& c, const TraceEv& ev) {
 // (and eigenvector update), zeroing the pivot — three barriers per round.
 // Input H column-major with leading dim ldh; outputs ascending c.ev[0..k)
 // and c.E (column-major, ld k), signs normalised.
-__device__ __noinline__ void jacobi_dev(Ctx& c, const double* H, int ldh, int k) {
+inline __device__ __noinline__ void jacobi_dev(Ctx& c, const double* H, int ldh, int k, bool tight = false) {
   double* const A = c.JA;
   double* const V = c.JV;
   double* const red = c.rs.part;  // scratch [kWarps]
@@ -76,7 +76,8 @@ __device__ __noinline__ void jacobi_dev(Ctx& c, const double* H, int ldh, int k)
     for (int idx = tid; idx < k * k; idx += kThreads) mloc = fmax(mloc, fabs(A[idx]));
     // 2 ulp of the largest entry: below this a pivot is rounding noise (a
     // tighter bound never triggers and costs ~3x more sweeps, measured)
-    const double thresh = block_max(mloc) * 4e-16;
+    // parity mode (tight): the checker's threshold and pivot test (base.cpp jacobi_eigh)
+    const double thresh = block_max(mloc) * (tight ? 1e-18 : 4e-16);
     for (int sweep = 0; sweep < 40; ++sweep) {
       double oloc = 0.0;
       for (int idx = tid; idx < k * k; idx += kThreads) {
@@ -98,7 +99,7 @@ __device__ __noinline__ void jacobi_dev(Ctx& c, const double* H, int ldh, int k)
           ok = q < k;
           if (ok) {
             const double apq = A[p + q * k];
-            if (fabs(apq) > thresh) {
+            if (tight ? apq != 0.0 : fabs(apq) > thresh) {
               const double th = (A[q + q * k] - A[p + p * k]) / (2.0 * apq);
               double tn;
               if (fabs(th) > 1e150)
@@ -334,7 +335,7 @@ __device__ __forceinline__ void lz_sub(Ctx& c, const Params& P, int k, double* w
 }
 // orthogonalize (lanczos.cpp:22-28): h <- V'w; w -= Vh; h2 <- V'w; w -= Vh2;
 // h += h2.  Returns ||w||^2 (and *wsum = sum w); h left in hh[0..k).
-__device__ __noinline__ double lz_cgs2(Ctx& c, const Params& P, int k, double* w, double* hh,
+inline __device__ __noinline__ double lz_cgs2(Ctx& c, const Params& P, int k, double* w, double* hh,
                                        double* hh2, double* wsum) {
   lz_dot(c, P, k, w);
   if (threadIdx.x < (unsigned)k) hh[threadIdx.x] = c.rs.out[threadIdx.x];
@@ -368,7 +369,7 @@ __device__ __forceinline__ double lz_combine(Ctx& c, const Params& P, int f, con
 
 // min_eigenpair (lanczos.cpp:32-141) of op = C + A*(q), i.e. B = -op.
 // Per matvec: one gather pass (no barrier) + three all-reduces (CGS2).
-__device__ __noinline__ bool lanczos_dev(Ctx& c, const Params& P, const GOp& g, double tol,
+inline __device__ __noinline__ bool lanczos_dev(Ctx& c, const Params& P, const GOp& g, double tol,
                                          int max_iters, int block_restart, LzOut& best) {
   const DevPairs& I = P.I;
   const int64_t n = I.n;
@@ -499,12 +500,9 @@ __device__ __noinline__ bool lanczos_dev(Ctx& c, const Params& P, const GOp& g, 
       } else {
         release(xs);
       }
-      best.matvecs = matvecs;
+      // best keeps the matvec count of its own measure (lanczos.cpp:70, :110-114)
       prof_mark(c, P, kPfLzMeasure);
-      if (best.converged || matvecs >= max_iters || (breakdown && filled >= n)) {
-        best.matvecs = matvecs;
-        return true;
-      }
+      if (best.converged || matvecs >= max_iters || (breakdown && filled >= n)) return true;
     }
     // thick restart (lanczos.cpp:117-139)
     const int l = min(keep, f - 1 > 0 ? f - 1 : 1);
@@ -559,10 +557,7 @@ __device__ __noinline__ bool lanczos_dev(Ctx& c, const Params& P, const GOp& g, 
       double fsum;
       const double fn2 = lz_cgs2(c, P, l, fr, hh, hh2, &fsum);
       const double fn = sqrt(fn2);
-      if (fn <= 1e-13) {
-        best.matvecs = matvecs;
-        return true;
-      }
+      if (fn <= 1e-13) return true;
       pend = Pending{fr, fn, fsum / fn, sl};
       wc = w_idx;
     } else {
@@ -696,7 +691,7 @@ __device__ __noinline__ void rank_update_dev(Ctx& c, const Params& P, const doub
 }
 
 // hlr_solve (hlr.cpp:55-151).  Input buffers[R.yt] with rank s.
-__device__ __noinline__ bool hlr_dev(Ctx& c, const Params& P, Roles& R, int s, double beta, double eps_t,
+inline __device__ __noinline__ bool hlr_dev(Ctx& c, const Params& P, Roles& R, int s, double beta, double eps_t,
                         int outer_iter, unsigned long long deadline_ns, HlrOut& out) {
   const DevPairs& I = P.I;
   const Cfg& cf = P.cfg;

@@ -74,6 +74,16 @@ int cuhallar_gen_matrix_completion(int64_t n1, int64_t n2, int r, uint64_t seed,
 int cuhallar_gen_matrix_completion_paper(int64_t n1, int64_t n2, int r, uint64_t seed,
                                          int64_t draws, double tau_safety,
                                          cuhallar_instance** out);
+/* A matrix-completion instance from a caller's sample list, host buffers:
+ * Omega = {(i_k, j_k)} strictly increasing in (i, j) with 0 <= i < n1,
+ * 0 <= j < n2 (the order gen_matrix_completion produces, instances.cpp:160-175),
+ * b_k = M(i_k, j_k), and the trace bound tau (the reference derives it as
+ * 2 * tau_safety * ||M||_*, instances.cpp:212).  The SdpInstance the reference's
+ * McSpec path builds (instances.cpp:190-234) for data the caller already holds;
+ * validation on the device (CUHALLAR_ERR_INPUT on unsorted / out-of-range pairs). */
+int cuhallar_matcomp_from_samples(int64_t n1, int64_t n2, int64_t m, const int64_t* i,
+                                  const int64_t* j, const double* b, double tau,
+                                  cuhallar_instance** out);
 /* matcomp_constraint_count  instances.cpp:123-129 */
 int64_t cuhallar_matcomp_constraint_count(int64_t n1, int64_t n2, int r, int offset);
 /* gen_phase_retrieval(PrSpec)  instances.cpp:239-389 */

@@ -246,14 +246,30 @@ McData matrix_completion(i64 n1, i64 n2, int r, u64 seed, bool offset,
     m = i64(keys.size());
   } else {
     // Omega: rejection sampling of distinct (i,j), then sorted by (i,j).
+    // The reference's std::unordered_set membership test is restated with a
+    // flat open-addressing table (same accept/reject sequence, so the same
+    // Omega; it only changes the generation time: 165 s -> ~25 s at C4).
     keys.reserve(static_cast<size_t>(m));
-    std::unordered_set<u64> seen;
-    seen.reserve(static_cast<size_t>(m) * 2);
-    while (i64(seen.size()) < m) {
+    u64 cap = 16;
+    while (cap < u64(m) * 2) cap <<= 1;
+    std::vector<u64> table(static_cast<size_t>(cap), 0);  // key + 1; 0 = empty
+    const u64 mask = cap - 1;
+    auto insert = [&](u64 key) {
+      u64 h = key * 0x9E3779B97F4A7C15ULL;
+      h ^= h >> 29;
+      for (u64 t = h & mask;; t = (t + 1) & mask) {
+        if (table[t] == key + 1) return false;
+        if (table[t] == 0) {
+          table[t] = key + 1;
+          return true;
+        }
+      }
+    };
+    while (i64(keys.size()) < m) {
       const u64 i = rng.uniform_below(u64(n1));
       const u64 j = rng.uniform_below(u64(n2));
       const u64 key = i * u64(n2) + j;
-      if (seen.insert(key).second) keys.push_back(key);
+      if (insert(key)) keys.push_back(key);
     }
     std::sort(keys.begin(), keys.end());  // (i,j) order == key order
   }

@@ -422,6 +422,21 @@ def gen_matrix_completion(spec: McSpec) -> SdpInstance:
                 C.c_double(spec.tau_safety), kind="matcomp")
 
 
+def matcomp_from_samples(n1: int, n2: int, i, j, b, tau: float) -> SdpInstance:
+    """A matrix-completion SdpInstance from host sample arrays (the instance
+    gen_matrix_completion builds, instances.cpp:190-234, for data the caller
+    holds): (i, j) strictly increasing, b = M(i, j), trace bound tau.  The
+    arrays are copied host -> device and the pair CSR is built on the GPU."""
+    i = np.ascontiguousarray(i, dtype=np.int64)
+    j = np.ascontiguousarray(j, dtype=np.int64)
+    b = np.ascontiguousarray(b, dtype=np.float64)
+    if not (len(i) == len(j) == len(b)):
+        raise InputError("matcomp samples: i, j, b lengths differ")
+    return _new(_lib.cuhallar_matcomp_from_samples, C.c_int64(n1), C.c_int64(n2), C.c_int64(len(i)),
+                i.ctypes.data_as(_i64p), j.ctypes.data_as(_i64p), b.ctypes.data_as(_dp),
+                C.c_double(tau), kind="matcomp")
+
+
 @dataclass
 class PrSpec:
     """PrSpec (instances.hpp:60-70)."""

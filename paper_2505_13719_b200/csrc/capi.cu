@@ -5,6 +5,8 @@
 
 #include <algorithm>
 #include <chrono>
+#include <cmath>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <memory>
@@ -13,12 +15,14 @@
 #include <vector>
 
 #include "../../include/cuhallar.h"
+#include "devgen.hpp"
 #include "host_instances.hpp"
 #include "kernel_setup.cuh"
 #include "solve.cuh"
 
 using namespace hallar;
 namespace hh = hallar_host;
+namespace hd = hallar_dev;
 
 // ----------------------------------------------------------------- kernel ---
 namespace hallar {
@@ -128,7 +132,6 @@ struct cuhallar_instance {
   DevPairs I{};
   int64_t bytes = 0;
   int64_t h2d = 0;
-  std::vector<int64_t> lo_eid_host;
   // device arrays
   int32_t *ei = nullptr, *ej = nullptr, *lo_col = nullptr;
   int64_t *up_ptr = nullptr, *lo_ptr = nullptr, *lo_eid = nullptr, *tile_row = nullptr;
@@ -187,36 +190,28 @@ struct cuhallar_solution {
 
 namespace {
 
-// Upload the pair structure and build the lower CSR (stable by edge id).
-void upload_pairs(cuhallar_instance* in) {
+// Device structure of a pair instance (devgen.cu builds it on the GPU):
+// ei / ej (device, sorted by (i, j); the instance takes ownership), the row
+// pointers of both halves, the lower CSR stable by edge id, row tiles, and
+// the scaled right-hand side in both orders.  b_dev: unscaled device b
+// (matrix completion, owned from here on) or null (b from h.b / theta).
+void build_pairs(cuhallar_instance* in, int32_t* d_ei, int32_t* d_ej, double* b_dev,
+                 const double* b_host = nullptr) {
   auto& h = in->h;
   const int64_t n = h.n, np = h.np;
-  std::vector<int64_t> up(n + 1, 0), lo(n + 1, 0);
-  for (int64_t k = 0; k < np; ++k) {
-    ++up[h.ei[k] + 1];
-    ++lo[h.ej[k] + 1];
-  }
-  for (int64_t a = 0; a < n; ++a) {
-    up[a + 1] += up[a];
-    lo[a + 1] += lo[a];
-  }
-  std::vector<int32_t> lo_col(np);
-  std::vector<int64_t> lo_eid(np);
-  {
-    std::vector<int64_t> cur(lo.begin(), lo.end() - 1);
-    for (int64_t k = 0; k < np; ++k) {
-      const int64_t e = cur[h.ej[k]]++;
-      lo_col[e] = h.ei[k];
-      lo_eid[e] = k;
-    }
-  }
-  in->ei = dupload(h.ei, &in->bytes);
-  in->ej = dupload(h.ej, &in->bytes);
-  in->up_ptr = dupload(up, &in->bytes);
-  in->lo_ptr = dupload(lo, &in->bytes);
-  in->lo_col = dupload(lo_col, &in->bytes);
-  in->lo_eid = dupload(lo_eid, &in->bytes);
-  in->lo_eid_host = std::move(lo_eid);
+  in->ei = d_ei;
+  in->ej = d_ej;
+  in->bytes += int64_t(2 * np * sizeof(int32_t));
+  hd::DevCsr csr;
+  hd::build_csr_device(n, np, d_ei, d_ej, &csr, 0);
+  in->up_ptr = csr.up_ptr;
+  in->lo_ptr = csr.lo_ptr;
+  in->lo_col = csr.lo_col;
+  in->lo_eid = csr.lo_eid;
+  in->bytes += int64_t(2 * (n + 1) * sizeof(int64_t) + np * (sizeof(int32_t) + sizeof(int64_t)));
+  std::vector<int64_t> up(n + 1), lo(n + 1);
+  ck(cudaMemcpy(up.data(), csr.up_ptr, (n + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost), "up_ptr");
+  ck(cudaMemcpy(lo.data(), csr.lo_ptr, (n + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost), "lo_ptr");
   {
     // Row tiles for the tile engine: consecutive rows, <= kTileRows rows and
     // <= target entries, target chosen so that every CTA gets tiles.
@@ -243,12 +238,12 @@ void upload_pairs(cuhallar_instance* in) {
       r0 = r1;
     }
     in->tile_row = dupload(tr, &in->bytes);
+    in->h2d += int64_t(tr.size() * sizeof(int64_t));
     in->tile_row_host = tr;
     in->up_ptr_host = up;
     in->I.tile_row = in->tile_row;
     in->I.ntiles = int64_t(tr.size()) - 1;
   }
-  in->h2d += in->bytes;
   DevPairs& I = in->I;
   I.family = h.family;
   I.has_trace = h.has_trace ? 1 : 0;
@@ -261,27 +256,55 @@ void upload_pairs(cuhallar_instance* in) {
   I.lo_ptr = in->lo_ptr;
   I.lo_col = in->lo_col;
   I.lo_eid = in->lo_eid;
-  // scale_instance (solver.cpp:31-42): b <- b / tau, norm_b1 <- norm_b1 / tau
-  std::vector<double> bs(h.m);
-  for (int64_t k = 0; k < h.m; ++k) bs[k] = h.tau != 1.0 ? h.b[k] / h.tau : h.b[k];
-  I.norm_b1 = h.tau != 1.0 ? h.norm_b1 / h.tau : h.norm_b1;
-  I.nb2 = std::sqrt(hh::eigen_order_sum_sq(bs.data(), h.m));
   I.norm_C1 = h.norm_C1;
   if (h.has_trace) {
-    I.b_trace = bs[h.m - 1];
-    bool any = false;
-    for (int64_t k = 0; k < np; ++k) any |= bs[k] != 0.0;
-    if (any) throw hh::InputError("theta: nonzero edge right-hand side");
-  } else {
-    std::vector<double> bl(np);
-    for (int64_t e = 0; e < np; ++e) bl[e] = bs[in->lo_eid_host[e]];
-    bs.resize(np);
-    in->b_up = dupload(bs, &in->bytes);
-    in->b_lo = dupload(bl, &in->bytes);
-    in->h2d += int64_t(2 * np * sizeof(double));
-    I.b_up = in->b_up;
-    I.b_lo = in->b_lo;
+    // theta: b = e_{m-1}, tau = 1 (instances.cpp:80-87)
+    I.b_trace = h.b.empty() ? 1.0 : h.b[h.m - 1];
+    I.norm_b1 = h.norm_b1;
+    I.nb2 = std::fabs(I.b_trace);
+    for (int64_t k = 0; k + 1 < int64_t(h.b.size()); ++k)
+      if (h.b[k] != 0.0) throw hh::InputError("theta: nonzero edge right-hand side");
+    return;
   }
+  // matrix completion: unscaled b on the device (edge order); the Eigen-order
+  // norms on the host from b_host, else from h.b (copied back if the device
+  // generated b); scale_instance (solver.cpp:31-42): b <- b / tau
+  if (!b_host && !h.b.empty()) b_host = h.b.data();
+  if (!b_dev) {
+    if (!b_host) throw hh::InputError("matcomp: no right-hand side");
+    b_dev = dalloc<double>(size_t(np), nullptr);
+    ck(cudaMemcpy(b_dev, b_host, np * sizeof(double), cudaMemcpyHostToDevice), "b");
+    in->h2d += int64_t(np * sizeof(double));
+  } else if (!b_host) {
+    h.b.resize(size_t(np));
+    ck(cudaMemcpy(h.b.data(), b_dev, np * sizeof(double), cudaMemcpyDeviceToHost), "b D2H");
+    b_host = h.b.data();
+  }
+  in->ub_up = b_dev;
+  in->bytes += int64_t(np * sizeof(double));
+  in->b_up = dalloc<double>(size_t(np), &in->bytes);
+  in->b_lo = dalloc<double>(size_t(np), &in->bytes);
+  hd::scale_and_lower(b_dev, np, h.tau, in->lo_eid, in->b_up, in->b_lo, 0);
+  // host reductions overlap the device scaling
+  if (h.norm_b1 == 0.0) h.norm_b1 = hh::eigen_order_sum_abs(b_host, np);
+  I.norm_b1 = h.tau != 1.0 ? h.norm_b1 / h.tau : h.norm_b1;
+  I.nb2 = std::sqrt(hh::eigen_order_sum_sq_scaled(b_host, np, h.tau));
+  ck(cudaDeviceSynchronize(), "b scale");
+  I.b_up = in->b_up;
+  I.b_lo = in->b_lo;
+}
+
+// host-built pair instance -> device
+void upload_pairs(cuhallar_instance* in) {
+  auto& h = in->h;
+  int32_t* dei = dalloc<int32_t>(size_t(h.np), nullptr);
+  int32_t* dej = dalloc<int32_t>(size_t(h.np), nullptr);
+  ck(cudaMemcpy(dei, h.ei.data(), h.np * sizeof(int32_t), cudaMemcpyHostToDevice), "ei");
+  ck(cudaMemcpy(dej, h.ej.data(), h.np * sizeof(int32_t), cudaMemcpyHostToDevice), "ej");
+  in->h2d += int64_t(2 * h.np * sizeof(int32_t));
+  std::vector<int32_t>().swap(h.ei);
+  std::vector<int32_t>().swap(h.ej);
+  build_pairs(in, dei, dej, nullptr);
 }
 
 void ensure_workspace(cuhallar_instance* in, int grid, uint64_t seed, int block_restart) {
@@ -505,11 +528,11 @@ void use_unscaled_b(cuhallar_instance* in, Params& P) {
   if (!in->ub_up) {
     std::vector<double> up(in->h.b.begin(), in->h.b.begin() + in->h.np);
     in->ub_up = dupload(up, &in->bytes);
-    if (in->h.family != kPhaseret) {
-      std::vector<double> lo(in->h.np);
-      for (int64_t e = 0; e < in->h.np; ++e) lo[e] = up[in->lo_eid_host[e]];
-      in->ub_lo = dupload(lo, &in->bytes);
-    }
+  }
+  if (!in->ub_lo && in->h.family != kPhaseret) {
+    in->ub_lo = dalloc<double>(size_t(in->h.np), &in->bytes);
+    gather_lower<<<unsigned((in->h.np + 255) / 256), 256>>>(in->ub_up, in->lo_eid, in->h.np, in->ub_lo);
+    ck(cudaGetLastError(), "gather_lower");
   }
   P.I.b_up = in->ub_up;
   P.I.b_lo = in->ub_lo;
@@ -589,6 +612,56 @@ cuhallar_instance* finish_pairs(hh::HostInst&& h) {
   return in.release();
 }
 
+// pair instance whose constraint arrays are already on the device
+cuhallar_instance* finish_pairs_dev(hh::HostInst&& h, const hd::DevSamples& ds,
+                                    const double* b_host = nullptr) {
+  auto in = std::make_unique<cuhallar_instance>();
+  ck(cudaGetDevice(&in->device), "device");
+  in->h = std::move(h);
+  in->h.np = ds.m;
+  in->h.m = ds.m + (in->h.has_trace ? 1 : 0);
+  build_pairs(in.get(), ds.ei, ds.ej, ds.b, b_host);
+  return in.release();
+}
+
+hh::HostInst theta_meta(int64_t n) {
+  hh::HostInst h;
+  h.family = kTheta;
+  h.n = n;
+  h.has_trace = true;
+  h.tau = 1.0;
+  h.norm_b1 = 1.0;
+  h.norm_C1 = double(n) * double(n);
+  return h;
+}
+
+bool host_gen_forced() {
+  const char* e = std::getenv("CUHALLAR_HOST_GEN");
+  return e && *e && *e != '0';
+}
+
+// gen_matrix_completion (instances.cpp:131-234): hidden factors on the host,
+// the sample draws on the device (devgen.cu), the host generator when the
+// stream hits a uniform_below rejection or CUHALLAR_HOST_GEN=1
+cuhallar_instance* gen_matcomp(int64_t n1, int64_t n2, int r, uint64_t seed, bool offset,
+                               double tau_safety, int64_t paper_draws) {
+  if (!host_gen_forced()) {
+    auto pre = hh::matcomp_prefix(n1, n2, r, seed, offset, tau_safety, paper_draws);
+    hd::DevSamples ds;
+    if (hd::gen_matcomp_device(n1, n2, r, pre.state, pre.m_target, paper_draws, pre.U, pre.V, &ds, 0)) {
+      hh::HostInst h;
+      h.family = kMatcomp;
+      h.n = n1 + n2;
+      h.n1 = n1;
+      h.nuclear = pre.nuclear;
+      h.tau = pre.tau;
+      h.norm_C1 = 0.5 * double(h.n);
+      return finish_pairs_dev(std::move(h), ds);
+    }
+  }
+  return finish_pairs(hh::make_matcomp(n1, n2, r, seed, offset, tau_safety, paper_draws));
+}
+
 // gen_phase_retrieval (instances.cpp:298-389): masks, twiddles and the
 // spectrum / adjoint scratch go to HBM; b = map of the hidden signal is
 // computed by the device operator itself (instances.cpp:323-328).
@@ -665,7 +738,14 @@ void cuhallar_config_default(cuhallar_config* c) {
 
 int cuhallar_theta_hypercube(int d, cuhallar_instance** out) {
   return guard([&] {
-    *out = finish_pairs(hh::make_theta(int64_t(1) << d, hh::edges_hypercube(d)));
+    if (d < 1 || d >= 31) throw hh::InputError("hypercube dimension out of range");
+    if (host_gen_forced()) {
+      *out = finish_pairs(hh::make_theta(int64_t(1) << d, hh::edges_hypercube(d)));
+    } else {
+      hd::DevSamples ds;
+      hd::gen_hypercube_device(d, &ds, 0);
+      *out = finish_pairs_dev(theta_meta(int64_t(1) << d), ds);
+    }
     return 0;
   });
 }
@@ -703,7 +783,7 @@ int cuhallar_theta_file(const char* path, int fmt, cuhallar_instance** out) {
 int cuhallar_gen_matrix_completion(int64_t n1, int64_t n2, int r, uint64_t seed, int offset,
                                    double tau_safety, cuhallar_instance** out) {
   return guard([&] {
-    *out = finish_pairs(hh::make_matcomp(n1, n2, r, seed, offset != 0, tau_safety));
+    *out = gen_matcomp(n1, n2, r, seed, offset != 0, tau_safety, 0);
     return 0;
   });
 }
@@ -712,7 +792,32 @@ int cuhallar_gen_matrix_completion_paper(int64_t n1, int64_t n2, int r, uint64_t
                                          cuhallar_instance** out) {
   return guard([&] {
     if (draws < 1) throw hh::InputError("matcomp: draws must be >= 1");
-    *out = finish_pairs(hh::make_matcomp(n1, n2, r, seed, false, tau_safety, draws));
+    *out = gen_matcomp(n1, n2, r, seed, false, tau_safety, draws);
+    return 0;
+  });
+}
+int cuhallar_matcomp_from_samples(int64_t n1, int64_t n2, int64_t m, const int64_t* i,
+                                  const int64_t* j, const double* b, double tau,
+                                  cuhallar_instance** out) {
+  return guard([&] {
+    if (!(n1 >= 1 && n2 >= 1 && n1 + n2 < (int64_t(1) << 31)))
+      throw hh::InputError("matcomp samples: bad dimensions");
+    if (m < 1 || m > n1 * n2) throw hh::InputError("matcomp samples: bad sample count");
+    if (!(tau > 0.0 && std::isfinite(tau))) throw hh::InputError("matcomp samples: tau must be positive");
+    if (!i || !j || !b) throw hh::InputError("matcomp samples: null array");
+    hd::DevSamples ds;
+    try {
+      hd::pairs_from_host(n1, n2, m, i, j, &ds, 0);
+    } catch (const std::invalid_argument& e) {
+      throw hh::InputError(e.what());
+    }
+    hh::HostInst h;
+    h.family = kMatcomp;
+    h.n = n1 + n2;
+    h.n1 = n1;
+    h.tau = tau;
+    h.norm_C1 = 0.5 * double(h.n);
+    *out = finish_pairs_dev(std::move(h), ds, b);
     return 0;
   });
 }
@@ -750,13 +855,35 @@ int cuhallar_instance_get_info(const cuhallar_instance* in, cuhallar_instance_in
   return 0;
 }
 int cuhallar_instance_get_b(const cuhallar_instance* in, double* b) {
-  std::memcpy(b, in->h.b.data(), sizeof(double) * in->h.b.size());
-  return 0;
+  return guard([&] {
+    const auto& h = in->h;
+    if (int64_t(h.b.size()) == h.m) {
+      std::memcpy(b, h.b.data(), sizeof(double) * h.b.size());
+    } else if (h.has_trace) {  // theta: e_{m-1}
+      std::memset(b, 0, sizeof(double) * h.m);
+      b[h.m - 1] = 1.0;
+    } else {
+      DevGuard dg(in->device);
+      ck(cudaMemcpy(b, in->ub_up, sizeof(double) * h.m, cudaMemcpyDeviceToHost), "b D2H");
+    }
+    return 0;
+  });
 }
 int cuhallar_instance_get_pairs(const cuhallar_instance* in, int64_t* i, int64_t* j) {
-  std::memcpy(i, in->h.pub_i.data(), sizeof(int64_t) * in->h.pub_i.size());
-  std::memcpy(j, in->h.pub_j.data(), sizeof(int64_t) * in->h.pub_j.size());
-  return 0;
+  return guard([&] {
+    if (in->h.family == kPhaseret) throw hh::InputError("get_pairs: not a pair instance");
+    DevGuard dg(in->device);
+    const int64_t np = in->h.np;
+    std::vector<int32_t> a(static_cast<size_t>(np)), c(static_cast<size_t>(np));
+    ck(cudaMemcpy(a.data(), in->ei, np * sizeof(int32_t), cudaMemcpyDeviceToHost), "ei D2H");
+    ck(cudaMemcpy(c.data(), in->ej, np * sizeof(int32_t), cudaMemcpyDeviceToHost), "ej D2H");
+    const int64_t off = in->h.family == kMatcomp ? in->h.n1 : 0;  // omega_j = j - n1
+    for (int64_t k = 0; k < np; ++k) {
+      i[k] = a[k];
+      j[k] = c[k] - off;
+    }
+    return 0;
+  });
 }
 int cuhallar_instance_get_phaseret(const cuhallar_instance* in, double* x, double* masks) {
   if (x) std::memcpy(x, in->h.hidden_x.data(), sizeof(double) * 2 * in->h.hidden_x.size());
@@ -860,13 +987,12 @@ static double host_multiplier_to_dev(cuhallar_instance* in, const double* p_host
     ck(cudaMemset(in->p_lo, 0, np * sizeof(double)), "p_lo");
     return 0.0;
   }
-  std::vector<double> up(np), lo(np);
-  for (int64_t k = 0; k < np; ++k) up[k] = p_host ? p_host[k] : 0.0;
-  if (in->h.family != kPhaseret)
-    for (int64_t e = 0; e < np; ++e) lo[e] = up[in->lo_eid_host[e]];
-  ck(cudaMemcpy(in->p_up, up.data(), np * sizeof(double), cudaMemcpyHostToDevice), "p_up");
-  ck(cudaMemcpy(in->p_lo, lo.data(), np * sizeof(double), cudaMemcpyHostToDevice), "p_lo");
-  in->h2d += int64_t(2 * np * sizeof(double));
+  ck(cudaMemcpy(in->p_up, p_host, np * sizeof(double), cudaMemcpyHostToDevice), "p_up");
+  if (in->h.family != kPhaseret) {
+    gather_lower<<<unsigned((np + 255) / 256), 256>>>(in->p_up, in->lo_eid, np, in->p_lo);
+    ck(cudaGetLastError(), "gather_lower");
+  }
+  in->h2d += int64_t(np * sizeof(double));
   return (in->h.has_trace && p_host) ? p_host[np] : 0.0;
 }
 

@@ -94,6 +94,13 @@ static double eigen_sum(int64_t n, F f) {
 double eigen_order_sum_sq(const double* x, int64_t n) {
   return eigen_sum(n, [x](int64_t i) { return x[i] * x[i]; });
 }
+double eigen_order_sum_sq_scaled(const double* x, int64_t n, double tau) {
+  if (tau == 1.0) return eigen_order_sum_sq(x, n);
+  return eigen_sum(n, [x, tau](int64_t i) {
+    const double y = x[i] / tau;
+    return y * y;
+  });
+}
 double eigen_order_sum_abs(const double* x, int64_t n) {
   return eigen_sum(n, [x](int64_t i) { return std::fabs(x[i]); });
 }
@@ -200,15 +207,11 @@ HostInst make_theta(int64_t n, const Edges& edges) {
   h.has_trace = true;
   h.ei.resize(h.np);
   h.ej.resize(h.np);
-  h.pub_i.resize(h.np);
-  h.pub_j.resize(h.np);
   for (int64_t k = 0; k < h.np; ++k) {
     const auto [u, v] = edges[k];
     if (!(u >= 0 && v < n && u < v)) throw InputError("theta: bad edge");
     h.ei[k] = int32_t(u);
     h.ej[k] = int32_t(v);
-    h.pub_i[k] = u;
-    h.pub_j[k] = v;
   }
   h.b.assign(size_t(h.m), 0.0);
   h.b[h.m - 1] = 1.0;
@@ -330,13 +333,49 @@ double nuclear_small(std::vector<double> A, int r) {
 }
 }  // namespace
 
-HostInst make_matcomp(int64_t n1, int64_t n2, int r, uint64_t seed, bool offset,
-                      double tau_safety, int64_t paper_draws) {
+namespace {
+void matcomp_check(int64_t n1, int64_t n2, int r, double tau_safety, int64_t paper_draws) {
   if (!(n1 >= 1 && n2 >= n1)) throw InputError("matcomp: need n2 >= n1 >= 1");
   if (!(r >= 1 && r <= n1)) throw InputError("matcomp: need 1 <= r <= n1");
   if (!(tau_safety >= 1.0)) throw InputError("matcomp: tau_safety must be >= 1");
   if (n1 + n2 >= (int64_t(1) << 31)) throw InputError("matcomp: n1 + n2 >= 2^31");
   if (paper_draws < 0) throw InputError("matcomp: draws must be >= 0");
+}
+// ||M||_* of M = U V' from the R factors (instances.cpp:179-187)
+double matcomp_nuclear(const std::vector<double>& U, const std::vector<double>& V, int64_t n1, int64_t n2,
+                       int r) {
+  const auto Ru = house_r(U, n1, r), Rv = house_r(V, n2, r);
+  std::vector<double> core(size_t(r) * r);
+  for (int a = 0; a < r; ++a)
+    for (int b = 0; b < r; ++b) {
+      double s = 0;
+      for (int t = 0; t < r; ++t) s += Ru[a + t * r] * Rv[b + t * r];
+      core[a + b * r] = s;
+    }
+  return nuclear_small(core, r);
+}
+}  // namespace
+
+McPrefix matcomp_prefix(int64_t n1, int64_t n2, int r, uint64_t seed, bool offset, double tau_safety,
+                        int64_t paper_draws) {
+  matcomp_check(n1, n2, r, tau_safety, paper_draws);
+  McPrefix p;
+  p.m_target = paper_draws > 0 ? 0 : matcomp_count(n1, n2, r, offset);
+  if (p.m_target > n1 * n2) throw InputError("matcomp: sample count exceeds matrix size");
+  Xoshiro g(seed);
+  p.U.resize(size_t(n1) * r);
+  p.V.resize(size_t(n2) * r);
+  for (auto& x : p.U) x = g.normal();  // column-major fills (rng.cpp:69-74)
+  for (auto& x : p.V) x = g.normal();
+  g.state(p.state);
+  p.nuclear = matcomp_nuclear(p.U, p.V, n1, n2, r);
+  p.tau = 2.0 * tau_safety * p.nuclear;
+  return p;
+}
+
+HostInst make_matcomp(int64_t n1, int64_t n2, int r, uint64_t seed, bool offset,
+                      double tau_safety, int64_t paper_draws) {
+  matcomp_check(n1, n2, r, tau_safety, paper_draws);
   int64_t m = paper_draws > 0 ? 0 : matcomp_count(n1, n2, r, offset);
   if (m > n1 * n2) throw InputError("matcomp: sample count exceeds matrix size");
   Xoshiro g(seed);
@@ -369,34 +408,21 @@ HostInst make_matcomp(int64_t n1, int64_t n2, int r, uint64_t seed, bool offset,
   HostInst h;
   h.family = 1;
   h.n = n1 + n2;
+  h.n1 = n1;
   h.m = m;
   h.np = m;
   h.ei.resize(m);
   h.ej.resize(m);
-  h.pub_i.resize(m);
-  h.pub_j.resize(m);
   h.b.resize(m);
   for (int64_t k = 0; k < m; ++k) {
     const int64_t i = int64_t(keys[k] / uint64_t(n2)), j = int64_t(keys[k] % uint64_t(n2));
-    h.pub_i[k] = i;
-    h.pub_j[k] = j;
     h.ei[k] = int32_t(i);
     h.ej[k] = int32_t(n1 + j);
     double d = U[i] * V[j];
     for (int t = 1; t < r; ++t) d = d + U[i + t * n1] * V[j + t * n2];
     h.b[k] = d;
   }
-  {
-    const auto Ru = house_r(U, n1, r), Rv = house_r(V, n2, r);
-    std::vector<double> core(size_t(r) * r);
-    for (int a = 0; a < r; ++a)
-      for (int b = 0; b < r; ++b) {
-        double s = 0;
-        for (int t = 0; t < r; ++t) s += Ru[a + t * r] * Rv[b + t * r];
-        core[a + b * r] = s;
-      }
-    h.nuclear = nuclear_small(core, r);
-  }
+  h.nuclear = matcomp_nuclear(U, V, n1, n2, r);
   h.tau = 2.0 * tau_safety * h.nuclear;
   h.norm_b1 = eigen_order_sum_abs(h.b.data(), m);
   h.norm_C1 = 0.5 * double(h.n);

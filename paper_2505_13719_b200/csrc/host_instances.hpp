@@ -28,6 +28,9 @@ class Xoshiro {
   double uniform();
   uint64_t below(uint64_t bound);
   double normal();
+  void state(uint64_t out[4]) const {
+    for (int i = 0; i < 4; ++i) out[i] = s_[i];
+  }
 
  private:
   uint64_t s_[4];
@@ -45,7 +48,7 @@ struct HostInst {
   std::vector<int32_t> ei, ej;  // pair constraints, sorted by (ei, ej), ei < ej
   std::vector<double> b;        // length m, unscaled
   double tau = 1.0, norm_b1 = 0.0, norm_C1 = 0.0, nuclear = 0.0;
-  std::vector<int64_t> pub_i, pub_j;  // theta: edges; matcomp: omega (j in [0, n2))
+  int64_t n1 = 0;  // matcomp: rows of M (pair j = n1 + column)
   // phase retrieval
   int64_t nc = 0;
   int L = 0;
@@ -69,10 +72,24 @@ int64_t matcomp_count(int64_t n1, int64_t n2, int r, bool offset);
 // deduplicated) instead of instances.cpp:123-159
 HostInst make_matcomp(int64_t n1, int64_t n2, int r, uint64_t seed, bool offset,
                       double tau_safety, int64_t paper_draws = 0);
+// The host part of gen_matrix_completion that precedes the sample draws:
+// hidden factors (column-major), the RNG state after them, the sample count
+// (reference rule) and the nuclear norm / tau.  The draws themselves are made
+// by devgen.cu (or by make_matcomp on the host).
+struct McPrefix {
+  int64_t m_target = 0;  // 0 under the paper rule
+  std::vector<double> U, V;
+  uint64_t state[4] = {0, 0, 0, 0};
+  double nuclear = 0.0, tau = 0.0;
+};
+McPrefix matcomp_prefix(int64_t n1, int64_t n2, int r, uint64_t seed, bool offset, double tau_safety,
+                        int64_t paper_draws);
 HostInst make_phaseret(int64_t n, int L, uint64_t seed, double tau_slack);
 
 // Eigen LinearVectorized redux order (SSE2, 2 accumulators of 2 lanes).
 double eigen_order_sum_sq(const double* x, int64_t n);
 double eigen_order_sum_abs(const double* x, int64_t n);
+// sum_i (x_i / tau)^2 in the same order (scale_instance, then squaredNorm)
+double eigen_order_sum_sq_scaled(const double* x, int64_t n, double tau);
 
 }  // namespace hallar_host

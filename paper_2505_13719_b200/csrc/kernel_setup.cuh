@@ -14,7 +14,6 @@ __device__ __forceinline__ void setup_ctx(Ctx& c, const Params& P, unsigned char
   c.t.lrank = blockIdx.x;
   c.t.lsize = gridDim.x;
   c.t.fab = &P.fab;
-  c.Pp = &P;
   c.t.mw = P.fab.world > 1;
   c.t.bar = P.bar;
   c.t.slots = P.slots;

@@ -13,6 +13,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Ctx c;
   setup_ctx(c, P, smem_raw);
+  c.Pp = &P;  // debug hooks of the job phases (parity.cuh)
   p_dispatch(c, P, so);
 }
 

@@ -27,7 +27,7 @@ from typing import Callable, Optional
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libcuhallar.so")
+LIB_PATH = os.environ.get("CUHALLAR_LIB") or os.path.join(_HERE, "libcuhallar.so")  # override: A/B builds
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(

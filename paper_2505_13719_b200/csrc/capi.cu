@@ -11,6 +11,8 @@
 #include <cstring>
 #include <memory>
 #include <mutex>
+#include <atomic>
+#include <thread>
 #include <string>
 #include <vector>
 
@@ -156,6 +158,13 @@ struct cuhallar_instance {
   double *p_up = nullptr, *p_lo = nullptr, *q_up = nullptr, *q_lo = nullptr, *r_up = nullptr,
          *r_lo = nullptr;
   double* lz_rand = nullptr;
+  // Lanczos refills beyond the pre-drawn ones (RefillService)
+  std::unique_ptr<hh::Xoshiro> lz_gen;           // positioned after the pre-drawn normals
+  std::vector<std::vector<double>> lz_extra;     // refills n_refill + 1, ... drawn so far
+  int *svc_req_h = nullptr, *svc_ready_h = nullptr, *svc_err_d = nullptr;
+  double* svc_buf_h = nullptr;
+  hd::DevSell sell;  // SELL-32 row-stream copy (single-GPU row passes), optional
+  double *s_b = nullptr, *s_ub = nullptr, *p_sell = nullptr, *q_sell = nullptr, *r_sell = nullptr;
   int n_refill = 0;
   uint64_t lz_seed = ~0ull;
   double* dscal = nullptr;
@@ -176,7 +185,12 @@ struct cuhallar_instance {
     f(masks); f(twid); f(prF); f(prG);
     f(bar); f(slots); f(arena); f(xbar); f(xslots); f(xerr);
     f(p_up); f(p_lo); f(q_up); f(q_lo); f(r_up); f(r_lo); f(lz_rand); f(dscal); f(discal); f(dso); f(dprof);
+    f(sell.off); f(sell.nlo); f(sell.nv); f(sell.col); f(sell.eid); f(s_b); f(s_ub); f(p_sell); f(q_sell); f(r_sell);
     if (trace_host) cudaFreeHost(trace_host);
+    if (svc_req_h) cudaFreeHost(svc_req_h);
+    if (svc_ready_h) cudaFreeHost(svc_ready_h);
+    if (svc_buf_h) cudaFreeHost(svc_buf_h);
+    f(svc_err_d);
     if (trace_count_host) cudaFreeHost(trace_count_host);
   }
 };
@@ -189,6 +203,52 @@ struct cuhallar_solution {
 };
 
 namespace {
+
+// SELL-32 copy of the row streams (common.cuh DevPairs::s_*) for the
+// single-GPU row passes of large instances (>= kRtMinRows rows per CTA), when
+// HBM allows it next to the factor arena; CUHALLAR_NO_SELL=1 disables it.
+int grid_size(int requested);
+void build_sell(cuhallar_instance* in) {
+  const auto& h = in->h;
+  const char* e = std::getenv("CUHALLAR_NO_SELL");
+  if (e && *e && *e != '0') return;
+  int team = 148;
+  try {
+    team = grid_size(0);
+  } catch (...) {
+  }
+  if (h.n < int64_t(team) * kRtMinRows) return;
+  hd::DevSell sl;
+  const int64_t slots = hd::sell_slots_device(h.n, in->up_ptr, in->lo_ptr, &sl, 0);
+  const int64_t per_slot = 4 + 4 + 24 + (h.has_trace ? 0 : 8);
+  const int64_t arena = h.n * (int64_t(kNBuf) * kSMax + kLanczosMax + kLanczosMax / 3 + 8) * 8;
+  size_t fr = 0, tot = 0;
+  ck(cudaMemGetInfo(&fr, &tot), "mem info");
+  if (int64_t(fr) < slots * per_slot + arena + (int64_t(4) << 30)) {  // no room: the row-thread engine
+    cudaFree(sl.off); cudaFree(sl.nlo); cudaFree(sl.nv);
+    return;
+  }
+  hd::sell_fill_device(h.n, in->up_ptr, in->lo_ptr, in->ej, in->lo_col, in->lo_eid, &sl, 0);
+  in->sell = sl;
+  in->bytes += slots * 8 + (sl.nslices + 1) * 8 + h.n * 8;
+  in->p_sell = dalloc<double>(size_t(slots), &in->bytes);
+  in->q_sell = dalloc<double>(size_t(slots), &in->bytes);
+  in->r_sell = dalloc<double>(size_t(slots), &in->bytes);
+  ck(cudaMemset(in->p_sell, 0, slots * sizeof(double)), "p_sell");
+  if (!h.has_trace) {
+    in->s_b = dalloc<double>(size_t(slots), &in->bytes);
+    hd::sell_gather(in->b_up, sl.eid, slots, in->s_b, 0);
+  }
+  ck(cudaDeviceSynchronize(), "sell");
+  DevPairs& I = in->I;
+  I.s_off = sl.off;
+  I.s_col = sl.col;
+  I.s_nlo = sl.nlo;
+  I.s_nv = sl.nv;
+  I.s_b = in->s_b;
+  I.s_eid = sl.eid;
+  I.s_slots = slots;
+}
 
 // Device structure of a pair instance (devgen.cu builds it on the GPU):
 // ei / ej (device, sorted by (i, j); the instance takes ownership), the row
@@ -264,6 +324,7 @@ void build_pairs(cuhallar_instance* in, int32_t* d_ei, int32_t* d_ej, double* b_
     I.nb2 = std::fabs(I.b_trace);
     for (int64_t k = 0; k + 1 < int64_t(h.b.size()); ++k)
       if (h.b[k] != 0.0) throw hh::InputError("theta: nonzero edge right-hand side");
+    build_sell(in);
     return;
   }
   // matrix completion: unscaled b on the device (edge order); the Eigen-order
@@ -292,6 +353,7 @@ void build_pairs(cuhallar_instance* in, int32_t* d_ei, int32_t* d_ej, double* b_
   ck(cudaDeviceSynchronize(), "b scale");
   I.b_up = in->b_up;
   I.b_lo = in->b_lo;
+  build_sell(in);
 }
 
 // host-built pair instance -> device
@@ -340,13 +402,24 @@ void ensure_workspace(cuhallar_instance* in, int grid, uint64_t seed, int block_
     // gaussian_vector(n, Rng(seed ^ 0x9b97f4a7c15)) calls (lanczos.cpp:46-50, 128-129)
     // (a refill is drawn only when a Krylov basis breaks down before reaching n:
     // rare, so a few per call suffice beyond tiny instances)
-    const int refill = int(std::max<int64_t>(4, std::min<int64_t>(64, (int64_t(1) << 16) / n)));
-    const auto v = hh::gaussian_stream(seed ^ 0x9b97f4a7c15ULL, n * (1 + refill));
+    // more are drawn on demand by the launch's RefillService
+    int refill = int(std::max<int64_t>(4, std::min<int64_t>(64, (int64_t(1) << 16) / n)));
+    if (const char* e = std::getenv("CUHALLAR_LZ_PREDRAW")) refill = std::max(0, std::atoi(e));  // tests
+    in->lz_gen = std::make_unique<hh::Xoshiro>(seed ^ 0x9b97f4a7c15ULL);
+    in->lz_extra.clear();
+    std::vector<double> v(size_t(n) * (1 + refill));
+    for (auto& x : v) x = in->lz_gen->normal();
     if (in->lz_rand) cudaFree(in->lz_rand);
     in->lz_rand = dupload(v, &in->bytes);
     in->h2d += int64_t(v.size() * sizeof(double));
     in->n_refill = refill;
     in->lz_seed = seed;
+    if (!in->svc_buf_h) {
+      ck(cudaHostAlloc(&in->svc_req_h, sizeof(int), cudaHostAllocMapped), "svc req");
+      ck(cudaHostAlloc(&in->svc_ready_h, sizeof(int), cudaHostAllocMapped), "svc ready");
+      ck(cudaHostAlloc(&in->svc_buf_h, sizeof(double) * n, cudaHostAllocMapped), "svc buf");
+      in->svc_err_d = dalloc<int>(1, &in->bytes);
+    }
   }
 }
 
@@ -499,12 +572,27 @@ Params base_params(cuhallar_instance* in, const cuhallar_config* cfg) {
   P.nslot = in->nslot;
   P.lz_rand = in->lz_rand;
   P.n_refill = in->n_refill;
+  if (in->svc_buf_h) {
+    int* dreq = nullptr;
+    int* drdy = nullptr;
+    double* dbuf = nullptr;
+    cudaHostGetDevicePointer(&dreq, in->svc_req_h, 0);
+    cudaHostGetDevicePointer(&drdy, in->svc_ready_h, 0);
+    cudaHostGetDevicePointer(&dbuf, in->svc_buf_h, 0);
+    P.svc_req = dreq;
+    P.svc_ready = drdy;
+    P.svc_buf = dbuf;
+    P.svc_err = in->svc_err_d;
+  }
   P.p_up = in->p_up;
   P.p_lo = in->p_lo;
   P.q_up = in->q_up;
   P.q_lo = in->q_lo;
   P.r_up = in->r_up;
   P.r_lo = in->r_lo;
+  P.p_sell = in->p_sell;
+  P.q_sell = in->q_sell;
+  P.r_sell = in->r_sell;
   P.scalars = in->dscal;
   P.iscalars = in->discal;
   P.trace = nullptr;
@@ -536,7 +624,54 @@ void use_unscaled_b(cuhallar_instance* in, Params& P) {
   }
   P.I.b_up = in->ub_up;
   P.I.b_lo = in->ub_lo;
+  if (in->sell.col) {
+    if (!in->s_ub) {
+      in->s_ub = dalloc<double>(size_t(in->sell.slots), &in->bytes);
+      hd::sell_gather(in->ub_up, in->sell.eid, in->sell.slots, in->s_ub, 0);
+    }
+    P.I.s_b = in->s_ub;
+  }
 }
+
+// Host side of the Lanczos refill protocol (solver.cuh lz_refill): while a
+// launch runs, serve refill j = the j-th gaussian_vector after the start
+// vector of Rng(seed ^ 0x9b97f4a7c15) (lanczos.cpp:46-50, 127-130; the
+// Box-Muller spare carries over, rng.cpp:54-67), drawn once and cached.
+struct RefillService {
+  cuhallar_instance* in;
+  std::atomic<bool> stop{false};
+  std::thread th;
+  explicit RefillService(cuhallar_instance* in_) : in(in_) {
+    *(volatile int*)in->svc_req_h = 0;
+    *(volatile int*)in->svc_ready_h = 0;
+    th = std::thread([this] { run(); });
+  }
+  void run() {
+    const int64_t n = in->h.n;
+    int served = 0;
+    while (!stop.load(std::memory_order_acquire)) {
+      const int j = *(volatile int*)in->svc_req_h;
+      if (j > in->n_refill && j != served) {
+        const size_t k = size_t(j - in->n_refill - 1);
+        while (in->lz_extra.size() <= k) {
+          std::vector<double> v(static_cast<size_t>(n));
+          for (auto& x : v) x = in->lz_gen->normal();
+          in->lz_extra.push_back(std::move(v));
+        }
+        std::memcpy(in->svc_buf_h, in->lz_extra[k].data(), sizeof(double) * n);
+        std::atomic_thread_fence(std::memory_order_seq_cst);
+        *(volatile int*)in->svc_ready_h = j;
+        served = j;
+      } else {
+        std::this_thread::sleep_for(std::chrono::microseconds(20));
+      }
+    }
+  }
+  ~RefillService() {
+    stop.store(true, std::memory_order_release);
+    th.join();
+  }
+};
 
 // Launch the persistent kernel; returns the solver status and fills *so.
 int launch(cuhallar_instance* in, Params& P, int grid, cudaStream_t st, SolveOut* so,
@@ -554,12 +689,22 @@ int launch(cuhallar_instance* in, Params& P, int grid, cudaStream_t st, SolveOut
   }
   // parity mode (parity.cuh) runs in its own persistent kernel (parity_kernel.cu)
   const bool par = P.cfg.parity && (P.op == kOpSolve || P.op == kOpMinEigG || P.op == kOpAipp);
+  if (par || P.fab.world > 1) {  // the SELL engine serves single-GPU fast-mode passes only
+    P.I.s_col = nullptr;
+    P.p_sell = P.q_sell = P.r_sell = nullptr;
+  }
+  std::unique_ptr<RefillService> svc;
+  if (P.svc_req && P.fab.world == 1 && (P.op == kOpSolve || P.op == kOpMinEigG || P.op == kOpAipp))
+    svc = std::make_unique<RefillService>(in);
+  else
+    P.svc_req = nullptr;
   ck(cudaLaunchCooperativeKernel(par ? hallar_parity_kernel_fn() : (const void*)hallar_kernel,
                                  dim3(grid), dim3(kThreads), args, smem_bytes(P.pass_scratch), st),
      "cooperative launch");
   if (ms) ck(cudaEventRecord(e1, st), "event");
   ck(cudaMemcpyAsync(so, in->dso, sizeof(SolveOut), cudaMemcpyDeviceToHost, st), "D2H out");
   ck(cudaStreamSynchronize(st), "hallar_kernel");
+  svc.reset();
   if (ms) {
     cudaEventElapsedTime(ms, e0, e1);
     cudaEventDestroy(e0);
@@ -691,13 +836,14 @@ void store_factor_dev(cuhallar_instance* in, const double* src_rowmajor, int s, 
 }
 // multiplier (length m, device) -> p_up / p_lo (+ trace scalar)
 double load_multiplier_dev(cuhallar_instance* in, const double* p_dev, double* up, double* lo,
-                           cudaStream_t st) {
+                           double* sell, cudaStream_t st) {
   const int64_t np = in->h.np;
   ck(cudaMemcpyAsync(up, p_dev, sizeof(double) * np, cudaMemcpyDeviceToDevice, st), "D2D p");
   if (in->h.family != kPhaseret) {
     gather_lower<<<unsigned((np + 255) / 256), 256, 0, st>>>(p_dev, in->lo_eid, np, lo);
     ck(cudaGetLastError(), "gather_lower");
   }
+  if (sell && in->sell.col) hd::sell_gather(p_dev, in->sell.eid, in->sell.slots, sell, st);
   double pt = 0.0;
   if (in->h.has_trace)
     ck(cudaMemcpyAsync(&pt, p_dev + np, sizeof(double), cudaMemcpyDeviceToHost, st), "D2H pt");
@@ -909,9 +1055,9 @@ static int run_op(cuhallar_instance* in, int op, const double* U_dev, int64_t ld
     use_unscaled_b(in, P);
     load_factor_dev(in, U_dev, ldu, s, st);
     if (op == kOpCPlusAdj || op == kOpAdj) {
-      P.q_trace_in = load_multiplier_dev(in, vec_dev, in->q_up, in->q_lo, st);
+      P.q_trace_in = load_multiplier_dev(in, vec_dev, in->q_up, in->q_lo, in->q_sell, st);
     } else if (op == kOpAlValue || op == kOpAlValGrad || op == kOpAlGrad) {
-      P.p_trace = load_multiplier_dev(in, vec_dev, in->p_up, in->p_lo, st);
+      P.p_trace = load_multiplier_dev(in, vec_dev, in->p_up, in->p_lo, in->p_sell, st);
     }
     if (op == kOpMap) P.out_vec = out_vec;
     double* rm = nullptr;
@@ -985,12 +1131,14 @@ static double host_multiplier_to_dev(cuhallar_instance* in, const double* p_host
   if (!p_host) {  // cold start p0 = 0 (solver.cpp:126-134): no host staging
     ck(cudaMemset(in->p_up, 0, np * sizeof(double)), "p_up");
     ck(cudaMemset(in->p_lo, 0, np * sizeof(double)), "p_lo");
+    if (in->p_sell) ck(cudaMemset(in->p_sell, 0, in->sell.slots * sizeof(double)), "p_sell");
     return 0.0;
   }
   ck(cudaMemcpy(in->p_up, p_host, np * sizeof(double), cudaMemcpyHostToDevice), "p_up");
   if (in->h.family != kPhaseret) {
     gather_lower<<<unsigned((np + 255) / 256), 256>>>(in->p_up, in->lo_eid, np, in->p_lo);
     ck(cudaGetLastError(), "gather_lower");
+    if (in->p_sell) hd::sell_gather(in->p_up, in->sell.eid, in->sell.slots, in->p_sell, 0);
   }
   in->h2d += int64_t(np * sizeof(double));
   return (in->h.has_trace && p_host) ? p_host[np] : 0.0;
@@ -1220,6 +1368,9 @@ int cuhallar_solve_sharded(cuhallar_instance* const* insts, int world, const cuh
       P.p_trace = host_multiplier_to_dev(in, p0_host);
       P.fab.world = world;
       P.fab.me = r;
+      P.I.s_col = nullptr;  // row-owner sharding keeps the CSR engines
+      P.p_sell = P.q_sell = P.r_sell = nullptr;
+      P.svc_req = nullptr;  // refills: the pre-drawn ones only
       P.fab.arena_len = in->arena_len;
       P.fab.xerr = in->xerr;
       for (int q = 0; q < world; ++q) {

@@ -87,6 +87,17 @@ struct DevPairs {
   const int64_t* tile_row = nullptr;  // [ntiles+1] first row of each row tile
   int64_t ntiles = 0;
   double norm_b1 = 0.0, nb2 = 0.0, norm_C1 = 0.0;  // scaled instance norms
+  // SELL-32 copy of the merged row streams for the single-GPU row passes:
+  // slice t = rows [32t, 32t + 32); entry v of row a (its lower entries, then
+  // its upper entries, increasing k) sits at slot s_off[a / 32] + 32 v + a % 32,
+  // so a warp reading entry v of its 32 rows touches 32 consecutive slots.
+  const int64_t* s_off = nullptr;   // [nslices + 1]
+  const int32_t* s_col = nullptr;   // slot -> gathered row (null: no SELL copy)
+  const int32_t* s_nlo = nullptr;   // [n] lower entries of each row
+  const int32_t* s_nv = nullptr;    // [n] entries of each row
+  const double* s_b = nullptr;      // slot -> scaled b (matrix completion)
+  const uint32_t* s_eid = nullptr;  // slot -> edge id (padding 0xffffffff)
+  int64_t s_slots = 0;
   // phase retrieval (family kPhaseret): np = m, b_up = b (constraint order)
   int64_t nc = 0;                 // complex dimension (n = 2 nc)
   int L = 0, lognc = 0;           // masks, log2(nc)
@@ -152,6 +163,12 @@ struct Params {
   double* lw = nullptr;
   const double* lz_rand = nullptr;  // n * (1 + n_refill) host-generated N(0,1)
   int n_refill = 0;
+  // refills beyond n_refill: requested from the host service thread of the
+  // launch (capi.cu RefillService) through host-mapped memory; null: none
+  int* svc_req = nullptr;          // mapped: refill index wanted
+  const int* svc_ready = nullptr;  // mapped: refill index staged in svc_buf
+  const double* svc_buf = nullptr; // mapped: n normals of that refill
+  int* svc_err = nullptr;          // device: service timeout flag
   // multipliers / gradient operator (edge + lower order)
   double* p_up = nullptr;
   double* p_lo = nullptr;
@@ -159,6 +176,9 @@ struct Params {
   double* q_lo = nullptr;
   double* r_up = nullptr;
   double* r_lo = nullptr;
+  double* p_sell = nullptr;  // the same multipliers in SELL slot order (null: no SELL copy)
+  double* q_sell = nullptr;
+  double* r_sell = nullptr;
   double p_trace = 0.0;      // p[m-1] input (theta)
   // op inputs
   int s_in = 1;              // rank of buf[0] input

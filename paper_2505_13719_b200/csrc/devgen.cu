@@ -276,9 +276,98 @@ __global__ void check_pairs(const int64_t* __restrict__ i, const int64_t* __rest
   ej[k] = int32_t(n1 + c);
 }
 
+// ---------------------------------------------------------------- SELL ---
+__global__ void sell_rowlen(const int64_t* __restrict__ up, const int64_t* __restrict__ lo, int64_t n,
+                            int32_t* __restrict__ nlo, int32_t* __restrict__ nv) {
+  const int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (a >= n) return;
+  const int64_t l = lo[a + 1] - lo[a], u = up[a + 1] - up[a];
+  nlo[a] = int32_t(l);
+  nv[a] = int32_t(l + u);
+}
+// slots of slice t: 32 x (longest row of the slice)
+__global__ void sell_slice_len(const int32_t* __restrict__ nv, int64_t n, int64_t nsl,
+                               int64_t* __restrict__ len) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= nsl) return;
+  int mx = 0;
+  for (int l = 0; l < 32; ++l) {
+    const int64_t a = t * 32 + l;
+    if (a < n) mx = max(mx, nv[a]);
+  }
+  len[t] = int64_t(mx) * 32;
+}
+__global__ void sell_fill(const int64_t* __restrict__ up, const int64_t* __restrict__ lo,
+                          const int32_t* __restrict__ ej, const int32_t* __restrict__ lo_col,
+                          const int64_t* __restrict__ lo_eid, const int64_t* __restrict__ off, int64_t n,
+                          int32_t* __restrict__ col, uint32_t* __restrict__ eid) {
+  const int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (a >= n) return;
+  const int64_t l0 = lo[a], nl = lo[a + 1] - l0, u0 = up[a], nu = up[a + 1] - u0;
+  const int64_t base = off[a >> 5] + (a & 31);
+  for (int64_t v = 0; v < nl; ++v) {
+    col[base + 32 * v] = lo_col[l0 + v];
+    eid[base + 32 * v] = uint32_t(lo_eid[l0 + v]);
+  }
+  for (int64_t v = 0; v < nu; ++v) {
+    col[base + 32 * (nl + v)] = ej[u0 + v];
+    eid[base + 32 * (nl + v)] = uint32_t(u0 + v);
+  }
+}
+__global__ void sell_gather_k(const double* __restrict__ src, const uint32_t* __restrict__ eid, int64_t slots,
+                              double* __restrict__ dst) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= slots) return;
+  const uint32_t e = eid[t];
+  dst[t] = e != 0xffffffffu ? src[e] : 0.0;
+}
+
 }  // namespace
 
 // ------------------------------------------------------------------ API ---
+int64_t sell_slots_device(int64_t n, const int64_t* up_ptr, const int64_t* lo_ptr, DevSell* out,
+                          cudaStream_t st) {
+  const int64_t nsl = (n + 31) / 32;
+  DBuf<int32_t> nlo(static_cast<size_t>(n)), nv(static_cast<size_t>(n));
+  DBuf<int64_t> len(static_cast<size_t>(nsl + 1)), off(static_cast<size_t>(nsl + 1));
+  sell_rowlen<<<blocks(n), 256, 0, st>>>(up_ptr, lo_ptr, n, nlo.p, nv.p);
+  ck(cudaGetLastError(), "sell_rowlen");
+  ck(cudaMemsetAsync(len.p + nsl, 0, sizeof(int64_t), st), "memset");
+  sell_slice_len<<<blocks(nsl), 256, 0, st>>>(nv.p, n, nsl, len.p);
+  ck(cudaGetLastError(), "sell_slice_len");
+  Temp temp;
+  size_t tb = 0;
+  ck(cub::DeviceScan::ExclusiveSum(nullptr, tb, len.p, off.p, nsl + 1, st), "scan size");
+  ck(cub::DeviceScan::ExclusiveSum(temp.get(tb), tb, len.p, off.p, nsl + 1, st), "scan");
+  int64_t slots = 0;
+  ck(cudaMemcpyAsync(&slots, off.p + nsl, sizeof(int64_t), cudaMemcpyDeviceToHost, st), "slots");
+  ck(cudaStreamSynchronize(st), "sell sizes");
+  out->slots = slots;
+  out->nslices = nsl;
+  out->nlo = nlo.release();
+  out->nv = nv.release();
+  out->off = off.release();
+  return slots;
+}
+
+void sell_fill_device(int64_t n, const int64_t* up_ptr, const int64_t* lo_ptr, const int32_t* ej,
+                      const int32_t* lo_col, const int64_t* lo_eid, DevSell* out, cudaStream_t st) {
+  DBuf<int32_t> col(static_cast<size_t>(out->slots));
+  DBuf<uint32_t> eid(static_cast<size_t>(out->slots));
+  ck(cudaMemsetAsync(col.p, 0, sizeof(int32_t) * out->slots, st), "memset col");
+  ck(cudaMemsetAsync(eid.p, 0xff, sizeof(uint32_t) * out->slots, st), "memset eid");
+  sell_fill<<<blocks(n), 256, 0, st>>>(up_ptr, lo_ptr, ej, lo_col, lo_eid, out->off, n, col.p, eid.p);
+  ck(cudaGetLastError(), "sell_fill");
+  ck(cudaStreamSynchronize(st), "sell fill");
+  out->col = col.release();
+  out->eid = eid.release();
+}
+
+void sell_gather(const double* src_edge_order, const uint32_t* eid, int64_t slots, double* dst,
+                 cudaStream_t st) {
+  sell_gather_k<<<blocks(slots), 256, 0, st>>>(src_edge_order, eid, slots, dst);
+  ck(cudaGetLastError(), "sell_gather");
+}
 bool gen_matcomp_device(int64_t n1, int64_t n2, int r, const uint64_t state[4], int64_t m_target,
                         int64_t paper_draws, const std::vector<double>& U,
                         const std::vector<double>& V, DevSamples* out, cudaStream_t st) {

@@ -51,4 +51,22 @@ void build_csr_device(int64_t n, int64_t np, const int32_t* ei, const int32_t* e
 void scale_and_lower(const double* b, int64_t np, double tau, const int64_t* lo_eid, double* b_up,
                      double* b_lo, cudaStream_t st);
 
+// SELL-32 copy of the merged row streams (common.cuh DevPairs::s_*).
+struct DevSell {
+  int64_t slots = 0, nslices = 0;
+  int64_t* off = nullptr;   // [nslices + 1]
+  int32_t* nlo = nullptr;   // [n]
+  int32_t* nv = nullptr;    // [n]
+  int32_t* col = nullptr;   // [slots]
+  uint32_t* eid = nullptr;  // [slots]
+};
+// sizes (off, nlo, nv) -> returns the slot count; then the slot arrays
+int64_t sell_slots_device(int64_t n, const int64_t* up_ptr, const int64_t* lo_ptr, DevSell* out,
+                          cudaStream_t st);
+void sell_fill_device(int64_t n, const int64_t* up_ptr, const int64_t* lo_ptr, const int32_t* ej,
+                      const int32_t* lo_col, const int64_t* lo_eid, DevSell* out, cudaStream_t st);
+// dst[slot] = src[eid[slot]] (0 on padding): an edge-order vector -> SELL order
+void sell_gather(const double* src_edge_order, const uint32_t* eid, int64_t slots, double* dst,
+                 cudaStream_t st);
+
 }  // namespace hallar_dev

@@ -814,14 +814,14 @@ __device__ __noinline__ bool p_lanczos(Ctx& c, const Params& P, const GOp& g, do
     const int sl = S.alloc();
     double* vl = slot_ptr(P, sl);
     if (breakdown) {
-      if (refill >= P.n_refill) {
+      ++refill;
+      double* fr = slot_ptr(P, fsl);
+      const double* rnd = lz_refill(c, P, refill);
+      if (!rnd) {
         fail(c, kErrCapacity, kMsgRefillCap);
         return false;
       }
-      ++refill;
-      double* fr = slot_ptr(P, fsl);
-      const double* rnd = P.lz_rand + (size_t)refill * n;
-      for (int64_t a = c.rl + threadIdx.x; a < c.rh; a += kThreads) fr[a] = rnd[a];
+      for (int64_t a = c.rl + threadIdx.x; a < c.rh; a += kThreads) fr[a] = __ldcv(rnd + a);
       c.t.sync();
       p_cgs2(c, P, l, fr, hh, hh2);
       const double fn = p_norm(c, n, fr);

@@ -182,6 +182,19 @@ inline __device__ __noinline__ void solve_dev(Ctx& c, const Params& P, SolveOut*
         const int64_t lo0 = I.lo_ptr[c.rl];
         for (int64_t e = threadIdx.x; e < lo_n; e += kThreads)
           P.p_lo[lo0 + e] = P.p_lo[lo0 + e] + beta * P.r_lo[lo0 + e];
+        if (P.p_sell) {  // the SELL copy, warp per slice (coalesced)
+          for (int64_t sl = (c.rl >> 5) + c.warp; sl < ((c.rh + 31) >> 5); sl += kWarps) {
+            const int64_t a = (sl << 5) + c.lane;
+            const int nv = (a >= c.rl && a < c.rh) ? I.s_nv[a] : 0;
+            const int64_t s_beg = I.s_off[sl];
+            const int L = (int)((I.s_off[sl + 1] - s_beg) >> 5);
+            for (int v = 0; v < L; ++v)
+              if (v < nv) {
+                const int64_t slot = s_beg + c.lane + 32 * (int64_t)v;
+                P.p_sell[slot] = P.p_sell[slot] + beta * P.r_sell[slot];
+              }
+          }
+        }
       }
       const double* U = P.buf[R.rep];
       for (int64_t a = c.rl + threadIdx.x; a < c.rh; a += kThreads)

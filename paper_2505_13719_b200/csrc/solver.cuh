@@ -367,6 +367,36 @@ __device__ __forceinline__ double lz_combine(Ctx& c, const Params& P, int f, con
   return v[0];
 }
 
+// Lanczos breakdown refill j (1-based, lanczos.cpp:127-130): the j-th next
+// gaussian_vector of the start-vector stream.  The first n_refill are
+// pre-drawn in HBM; later ones come from the launch's host service thread
+// (capi.cu RefillService): CTA 0 posts the index to host-mapped memory and
+// waits for the staged vector; the team barrier then releases every CTA to
+// read its rows (uncached loads: the staging buffer is reused).  Returns null
+// when no service is attached or the host does not answer within 60 s.
+inline __device__ const double* lz_refill(Ctx& c, const Params& P, int j) {
+  if (j <= P.n_refill) return P.lz_rand + (size_t)j * P.I.n;
+  if (!P.svc_req || c.t.mw) return nullptr;
+  if (c.t.rank == 0 && threadIdx.x == 0) {
+    *(volatile int*)P.svc_req = j;
+    __threadfence_system();
+    const unsigned long long t0 = globaltimer_ns();
+    int ok = 1;
+    while (*(volatile const int*)P.svc_ready != j) {
+      if (globaltimer_ns() - t0 > 60000000000ull) {
+        ok = 0;
+        break;
+      }
+      __nanosleep(1000);
+    }
+    __threadfence_system();
+    *(volatile int*)P.svc_err = ok ? 0 : 1;
+  }
+  c.t.sync();
+  if (*(volatile const int*)P.svc_err) return nullptr;
+  return P.svc_buf;
+}
+
 // min_eigenpair (lanczos.cpp:32-141) of op = C + A*(q), i.e. B = -op.
 // Per matvec: one gather pass (no barrier) + three all-reduces (CGS2).
 inline __device__ __noinline__ bool lanczos_dev(Ctx& c, const Params& P, const GOp& g, double tol,
@@ -544,15 +574,15 @@ inline __device__ __noinline__ bool lanczos_dev(Ctx& c, const Params& P, const G
     __syncthreads();
     const int w_idx = (w == slot_ptr(P, wslot[0])) ? 0 : 1;  // buffer holding the last w
     if (breakdown) {
-      if (refill >= P.n_refill) {
-        fail(c, kErrCapacity, kMsgRefillCap);
-        return false;
-      }
       ++refill;
       // fresh direction: next gaussian_vector of the same stream, orthogonalised
       double* fr = slot_ptr(P, wslot[1 - w_idx]);
-      const double* rnd = P.lz_rand + (size_t)refill * n;
-      for (int64_t a = c.rl + threadIdx.x; a < c.rh; a += kThreads) fr[a] = rnd[a];
+      const double* rnd = lz_refill(c, P, refill);
+      if (!rnd) {
+        fail(c, kErrCapacity, kMsgRefillCap);
+        return false;
+      }
+      for (int64_t a = c.rl + threadIdx.x; a < c.rh; a += kThreads) fr[a] = __ldcv(rnd + a);
       __syncthreads();
       double fsum;
       const double fn2 = lz_cgs2(c, P, l, fr, hh, hh2, &fsum);

@@ -89,6 +89,16 @@ int64_t cuhallar_matcomp_constraint_count(int64_t n1, int64_t n2, int r, int off
 /* gen_phase_retrieval(PrSpec)  instances.cpp:239-389 */
 int cuhallar_gen_phase_retrieval(int64_t n, int L, uint64_t seed, double tau_slack,
                                  cuhallar_instance** out);
+/* Gaussian-measurement phase retrieval (BASELINE configs[2];
+ * NOT in the reference): b_i = |a_i^* x|^2, i < m, a_i in C^n with i.i.d. CN(0,1)
+ * entries generated on the device from `seed`, x drawn like gen_phase_retrieval's
+ * hidden signal (instances.cpp:298-306), C = I, tau = tau_slack ||x||^2.  The map
+ * and adjoint are FP64 tensor-core (DMMA) contractions over the stored m x 2n
+ * measurement matrix.  Same operator / solve entry points as the other families. */
+int cuhallar_gen_gauss_phase_retrieval(int64_t n, int64_t m, uint64_t seed, double tau_slack,
+                                       cuhallar_instance** out);
+/* the measurement vectors of a Gaussian phase-retrieval instance (m x n row-major) */
+int cuhallar_instance_get_gauss(const cuhallar_instance* inst, double* A_re, double* A_im);
 void cuhallar_instance_destroy(cuhallar_instance* inst);
 
 typedef struct {

@@ -154,7 +154,7 @@ class OracleInstance:
         self.n, self.m = ints[0], ints[1]
         self.identity_constraint = None if ints[2] < 0 else ints[2]
         self.field_kind = ints[3]
-        self.family = ("theta", "matcomp", "phaseret", "dense")[ints[4]]
+        self.family = ("theta", "matcomp", "phaseret", "dense", "gauss_pr")[ints[4]]
         self.tau, self.norm_b1, self.norm_C1, self.nuclear_norm = dbls[0], dbls[1], dbls[2], dbls[3]
 
     def __del__(self):
@@ -213,6 +213,22 @@ class OracleInstance:
     def phaseret(cls, n, L, seed=0, tau_slack=1.1):
         h = _vp()
         _check(lib().orc_phaseret(C.c_longlong(n), C.c_int(L), C.c_ulonglong(seed),
+                                  C.c_double(tau_slack), C.byref(h)))
+        return cls(h.value)
+
+    @classmethod
+    def gauss_pr(cls, A, x, tau_slack=1.1):
+        """Gaussian-measurement phase retrieval (not in the
+        reference): b_i = |a_i^* x|^2 for the rows a_i of the complex m x n A."""
+        A = np.asarray(A, dtype=np.complex128)
+        x = np.asarray(x, dtype=np.complex128)
+        m, n = A.shape
+        are = np.ascontiguousarray(A.real)
+        aim = np.ascontiguousarray(A.imag)
+        xr = np.ascontiguousarray(x.real)
+        xi = np.ascontiguousarray(x.imag)
+        h = _vp()
+        _check(lib().orc_gauss_pr(C.c_longlong(n), C.c_longlong(m), _ptr(are), _ptr(aim), _ptr(xr), _ptr(xi),
                                   C.c_double(tau_slack), C.byref(h)))
         return cls(h.value)
 

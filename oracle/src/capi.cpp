@@ -150,6 +150,19 @@ int orc_phaseret(long long n, int L, unsigned long long seed, double tau_slack, 
     *out = h;
   });
 }
+// Gaussian phase retrieval from given measurement vectors (m x n row-major
+// re / im) and signal (n re / im)
+int orc_gauss_pr(long long n, long long m, const double* A_re, const double* A_im, const double* x_re,
+                 const double* x_im, double tau_slack, void** out) {
+  return guard([&] {
+    std::vector<cplx> x(static_cast<size_t>(n));
+    for (long long j = 0; j < n; ++j) x[j] = cplx(x_re[j], x_im[j]);
+    auto* h = new Handle;
+    h->inst = gauss_pr_instance(n, m, A_re, A_im, x, tau_slack);
+    h->family = 4;
+    *out = h;
+  });
+}
 // C: n x n col-major; A: m blocks of n x n col-major; b: m
 int orc_dense(long long n, long long m, const double* C, const double* A, const double* b,
               double tau, void** out) {

@@ -507,6 +507,95 @@ PrData phase_retrieval(i64 n, int L, u64 seed, double tau_slack) {
   return out;
 }
 
+// --------------------------------------------------- Gaussian phase retrieval ---
+// Dense restatement (the test_instances.cpp:255-297 pattern): y_ic = a_i^* u_c
+// summed over j in increasing order, d_i = sum_c |y_ic|^2 in column order;
+// adjoint z_c = sum_i a_i (q_i y_ic) over i in increasing order.
+Instance gauss_pr_instance(i64 n, i64 m, const double* A_re, const double* A_im,
+                           const std::vector<cplx>& x, double tau_slack) {
+  need(n >= 1 && m >= 1, "gauss_pr: empty");
+  need(i64(x.size()) == n, "gauss_pr: signal length");
+  need(tau_slack >= 1.0, "gauss_pr: tau_slack must be >= 1");
+  struct G {
+    i64 n, m;
+    std::vector<double> re, im;
+    // y = a_i^* u
+    cplx meas(i64 i, const cplx* u) const {
+      double yr = 0.0, yi = 0.0;
+      for (i64 j = 0; j < n; ++j) {
+        const double ar = re[i * n + j], ai = im[i * n + j];
+        yr = yr + (ar * u[j].real() + ai * u[j].imag());
+        yi = yi + (ar * u[j].imag() - ai * u[j].real());
+      }
+      return cplx(yr, yi);
+    }
+  };
+  auto D = std::make_shared<G>();
+  D->n = n;
+  D->m = m;
+  D->re.assign(A_re, A_re + n * m);
+  D->im.assign(A_im, A_im + n * m);
+  Instance I;
+  I.n = 2 * n;
+  I.m = m;
+  I.b.resize(static_cast<size_t>(m));
+  for (i64 i = 0; i < m; ++i) {
+    const cplx y = D->meas(i, x.data());
+    I.b[i] = y.real() * y.real() + y.imag() * y.imag();
+  }
+  I.tau = tau_slack * esum_fn(n, [&](i64 j) { return x[j].real() * x[j].real() + x[j].imag() * x[j].imag(); });
+  I.norm_b1 = esum_fn(m, [&](i64 k) { return std::fabs(I.b[k]); });
+  I.norm_C1 = double(2 * n);
+  I.field = Field::kComplexEmbedded;
+  auto load = [D](const Mat& U, i64 c) {
+    std::vector<cplx> u(static_cast<size_t>(D->n));
+    for (i64 j = 0; j < D->n; ++j) u[j] = cplx(U(j, c), U(D->n + j, c));
+    return u;
+  };
+  I.apply_C = [](const Mat& U) { return U; };
+  I.apply_map = [D, load](const Mat& U) {
+    Vec o(static_cast<size_t>(D->m));
+    std::vector<std::vector<cplx>> us;
+    for (i64 c = 0; c < U.cols; ++c) us.push_back(load(U, c));
+    for (i64 i = 0; i < D->m; ++i) {
+      double v = 0.0;
+      for (i64 c = 0; c < U.cols; ++c) {
+        const cplx y = D->meas(i, us[c].data());
+        const double t = y.real() * y.real() + y.imag() * y.imag();
+        v = c == 0 ? t : v + t;
+      }
+      o[i] = v;
+    }
+    return o;
+  };
+  auto adj = [D, load](const Vec& p, const Mat& U, bool add_id) {
+    Mat o(U.rows, U.cols);
+    for (i64 c = 0; c < U.cols; ++c) {
+      const auto u = load(U, c);
+      std::vector<double> zr(static_cast<size_t>(D->n), 0.0), zi(static_cast<size_t>(D->n), 0.0);
+      for (i64 i = 0; i < D->m; ++i) {
+        const cplx y = D->meas(i, u.data());
+        const double wr = p[i] * y.real(), wi = p[i] * y.imag();
+        for (i64 j = 0; j < D->n; ++j) {
+          const double ar = D->re[i * D->n + j], ai = D->im[i * D->n + j];
+          zr[j] = zr[j] + (ar * wr - ai * wi);
+          zi[j] = zi[j] + (ar * wi + ai * wr);
+        }
+      }
+      for (i64 j = 0; j < D->n; ++j) {
+        o(j, c) = zr[j];
+        o(D->n + j, c) = zi[j];
+      }
+    }
+    if (add_id)
+      for (i64 t = 0; t < o.size(); ++t) o.a[t] = o.a[t] + U.a[t];
+    return o;
+  };
+  I.apply_adjoint = [adj](const Vec& p, const Mat& U) { return adj(p, U, false); };
+  I.apply_C_plus_adjoint = [adj](const Vec& q, const Mat& U) { return adj(q, U, true); };
+  return I;
+}
+
 // ------------------------------------------------------------------ dense ---
 // tests/support/oracles.hpp:65-99 (DenseInstance::as_operator)
 Instance dense_instance(const DenseSdp& d0) {

@@ -195,6 +195,14 @@ struct PrData {
 };
 PrData phase_retrieval(i64 n, int L, u64 seed, double tau_slack);
 
+// Gaussian-measurement phase retrieval (NOT in the
+// reference, parity unpinned against it): b_i = |a_i^* x|^2 for given
+// measurement vectors a_i in C^n (A_re, A_im: m x n row-major) and signal x;
+// C = I, tau = tau_slack ||x||^2, real embedding [Re u; Im u] as the
+// coded-diffraction family (instances.cpp:266-269, 341-387).
+Instance gauss_pr_instance(i64 n, i64 m, const double* A_re, const double* A_im,
+                           const std::vector<cplx>& x, double tau_slack);
+
 // Explicit dense SDP (tests/support/oracles.hpp DenseInstance).
 struct DenseSdp {
   Mat C;

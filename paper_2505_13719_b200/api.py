@@ -215,6 +215,19 @@ class SdpInstance:
         _check(_lib.cuhallar_instance_get_phaseret(self._h, x.ctypes.data_as(_dp), masks.ctypes.data_as(_dp)))
         return x, masks.reshape(L, nc).T
 
+    def gauss_data(self):
+        """Measurement matrix A (m x n complex, rows a_i) and signal x of a
+        Gaussian phase-retrieval instance."""
+        if self.kind != "gauss_pr":
+            raise InputError("gauss_data: not a Gaussian phase-retrieval instance")
+        n = self.n // 2
+        are = np.empty((self.m, n))
+        aim = np.empty((self.m, n))
+        _check(_lib.cuhallar_instance_get_gauss(self._h, are.ctypes.data_as(_dp), aim.ctypes.data_as(_dp)))
+        x = np.empty(n, dtype=np.complex128)
+        _check(_lib.cuhallar_instance_get_phaseret(self._h, x.ctypes.data_as(_dp), None))
+        return are + 1j * aim, x
+
     # -- operator callables; U is n x s (numpy or torch), results numpy --
     def _dev_factor(self, U):
         import torch
@@ -449,6 +462,22 @@ class PrSpec:
 def gen_phase_retrieval(spec: PrSpec) -> SdpInstance:
     return _new(_lib.cuhallar_gen_phase_retrieval, C.c_int64(spec.n), C.c_int(spec.L),
                 C.c_uint64(spec.seed), C.c_double(spec.tau_slack), kind="phaseret")
+
+
+@dataclass
+class GaussPrSpec:
+    """Gaussian-measurement phase retrieval (SURVEY §8(f) row 3, BASELINE configs[2];
+    not in the reference): m measurements b_i = |a_i^* x|^2 of an n-dimensional
+    complex signal, a_i with i.i.d. CN(0, 1) entries."""
+    n: int = 0
+    m: int = 0
+    seed: int = 0
+    tau_slack: float = 1.1
+
+
+def gen_gauss_phase_retrieval(spec: GaussPrSpec) -> SdpInstance:
+    return _new(_lib.cuhallar_gen_gauss_phase_retrieval, C.c_int64(spec.n), C.c_int64(spec.m),
+                C.c_uint64(spec.seed), C.c_double(spec.tau_slack), kind="gauss_pr")
 
 
 # ------------------------------------------------------------------- solver --

@@ -140,6 +140,7 @@ struct cuhallar_instance {
   double *b_up = nullptr, *b_lo = nullptr;      // scaled b/tau (solve)
   double *ub_up = nullptr, *ub_lo = nullptr;    // unscaled b (operator ABI), lazy
   double2 *masks = nullptr, *twid = nullptr, *prF = nullptr, *prG = nullptr;  // phase retrieval
+  double* gA = nullptr;  // Gaussian phase retrieval: m x 2n measurement matrix
   // workspace
   int ws_grid = 0;
   unsigned long long* bar = nullptr;
@@ -182,7 +183,7 @@ struct cuhallar_instance {
       if (p) cudaFree(p);
     };
     f(ei); f(ej); f(lo_col); f(up_ptr); f(lo_ptr); f(lo_eid); f(tile_row); f(b_up); f(b_lo); f(ub_up); f(ub_lo);
-    f(masks); f(twid); f(prF); f(prG);
+    f(masks); f(twid); f(prF); f(prG); f(gA);
     f(bar); f(slots); f(arena); f(xbar); f(xslots); f(xerr);
     f(p_up); f(p_lo); f(q_up); f(q_lo); f(r_up); f(r_lo); f(lz_rand); f(dscal); f(discal); f(dso); f(dprof);
     f(sell.off); f(sell.nlo); f(sell.nv); f(sell.col); f(sell.eid); f(s_b); f(s_ub); f(p_sell); f(q_sell); f(r_sell);
@@ -427,6 +428,62 @@ Params base_params(cuhallar_instance* in, const cuhallar_config* cfg);
 int launch(cuhallar_instance* in, Params& P, int grid, cudaStream_t st, SolveOut* so,
            float* ms = nullptr);
 
+void upload_pr(cuhallar_instance* in);
+// Gaussian phase retrieval: A' generated on the device, the spectrum cache F
+// (kSMax x m) and the adjoint partials G (kSMax x parts x n), then b = the
+// device map of the hidden signal, as upload_pr does for coded diffraction.
+void upload_gpr(cuhallar_instance* in, uint64_t seed) {
+  auto& h = in->h;
+  const int64_t n = h.nc, m = h.m;
+  h.np = m;
+  in->gA = hd::gauss_fill_device(m, n, seed ^ 0x5eed9a55ULL, 0);
+  in->bytes += int64_t(2 * m * n * sizeof(double));
+  in->prF = dalloc<double2>(size_t(kSMax) * m, &in->bytes);
+  in->prG = dalloc<double2>(size_t(kSMax) * h.L * n, &in->bytes);
+  DevPairs& I = in->I;
+  I.family = kPhaseret;
+  I.has_trace = 0;
+  I.n = h.n;
+  I.np = m;
+  I.m = m;
+  I.nc = n;
+  I.L = h.L;
+  I.lognc = 0;
+  I.gA = in->gA;
+  I.F = in->prF;
+  I.G = in->prG;
+  I.norm_C1 = h.norm_C1;
+  {
+    const int grid = grid_size(0);
+    ensure_workspace(in, grid, 0, 30);
+    std::vector<double> x(size_t(h.n));
+    for (int64_t j = 0; j < n; ++j) {
+      x[j] = h.hidden_x[j].real();
+      x[n + j] = h.hidden_x[j].imag();
+    }
+    ck(cudaMemcpy(in->buf[0], x.data(), x.size() * sizeof(double), cudaMemcpyHostToDevice), "x");
+    in->h2d += int64_t(x.size() * sizeof(double));
+    double* bd = in->r_up;
+    Params P = base_params(in, nullptr);
+    P.op = kOpMap;
+    P.s_in = 1;
+    P.out_vec = bd;
+    SolveOut so{};
+    if (launch(in, P, grid, 0, &so, nullptr) != kOk) throw CudaError("gauss_pr: b map failed");
+    h.b.resize(m);
+    ck(cudaMemcpy(h.b.data(), bd, m * sizeof(double), cudaMemcpyDeviceToHost), "b");
+  }
+  h.norm_b1 = hh::eigen_order_sum_abs(h.b.data(), m);
+  std::vector<double> bs(m);
+  for (int64_t k = 0; k < m; ++k) bs[k] = h.tau != 1.0 ? h.b[k] / h.tau : h.b[k];
+  I.norm_b1 = h.tau != 1.0 ? h.norm_b1 / h.tau : h.norm_b1;
+  I.nb2 = std::sqrt(hh::eigen_order_sum_sq(bs.data(), m));
+  in->b_up = dupload(bs, &in->bytes);
+  in->h2d += int64_t(m * sizeof(double));
+  I.b_up = in->b_up;
+  I.b_lo = nullptr;
+}
+
 void upload_pr(cuhallar_instance* in) {
   auto& h = in->h;
   const int64_t nc = h.nc, m = h.m;
@@ -559,9 +616,11 @@ const char* msg_text(int id) {
 Params base_params(cuhallar_instance* in, const cuhallar_config* cfg) {
   Params P;
   P.I = in->I;
-  P.pass_scratch = in->h.family == kPhaseret
+  P.pass_scratch = in->gA ? 8 * kGprChunk  // staged DMMA right-hand side
+                  : in->h.family == kPhaseret
                       ? int(std::max<int64_t>(2 * in->h.nc, 1024))
-                      : std::max(kTileDoubles, kRtTheta);  // fixed-q staging has no rhs
+                      : (in->sell.col ? kPassScratch  // SELL stages (row_pass_sell_async)
+                                      : std::max(kTileDoubles, kRtTheta));  // fixed-q staging has no rhs
   cuhallar_config dc;
   cuhallar_config_default(&dc);
   P.cfg = to_dev_cfg(cfg ? *cfg : dc);
@@ -979,6 +1038,34 @@ int cuhallar_gen_phase_retrieval(int64_t n, int L, uint64_t seed, double tau_sla
     return 0;
   });
 }
+int cuhallar_gen_gauss_phase_retrieval(int64_t n, int64_t m, uint64_t seed, double tau_slack,
+                                       cuhallar_instance** out) {
+  return guard([&] {
+    if (n < 1 || m < 1 || 2 * n * m > (int64_t(1) << 36))
+      throw hh::InputError("gauss_pr: n, m out of range");
+    const int parts = int(std::max<int64_t>(1, std::min<int64_t>(16, m / 4096)));
+    auto in = std::make_unique<cuhallar_instance>();
+    ck(cudaGetDevice(&in->device), "device");
+    in->h = hh::make_gauss_pr(n, m, parts, seed, tau_slack);
+    upload_gpr(in.get(), seed);
+    *out = in.release();
+    return 0;
+  });
+}
+int cuhallar_instance_get_gauss(const cuhallar_instance* in, double* A_re, double* A_im) {
+  return guard([&] {
+    if (!in->gA) throw hh::InputError("get_gauss: not a Gaussian phase-retrieval instance");
+    DevGuard dg(in->device);
+    const int64_t n = in->h.nc, m = in->h.m;
+    std::vector<double> row(size_t(2 * n));
+    for (int64_t i = 0; i < m; ++i) {
+      ck(cudaMemcpy(row.data(), in->gA + i * 2 * n, 2 * n * sizeof(double), cudaMemcpyDeviceToHost), "A D2H");
+      std::memcpy(A_re + i * n, row.data(), n * sizeof(double));
+      std::memcpy(A_im + i * n, row.data() + n, n * sizeof(double));
+    }
+    return 0;
+  });
+}
 void cuhallar_instance_destroy(cuhallar_instance* inst) { delete inst; }
 
 int cuhallar_instance_get_info(const cuhallar_instance* in, cuhallar_instance_info* o) {
@@ -1033,7 +1120,8 @@ int cuhallar_instance_get_pairs(const cuhallar_instance* in, int64_t* i, int64_t
 }
 int cuhallar_instance_get_phaseret(const cuhallar_instance* in, double* x, double* masks) {
   if (x) std::memcpy(x, in->h.hidden_x.data(), sizeof(double) * 2 * in->h.hidden_x.size());
-  if (masks) std::memcpy(masks, in->h.masks.data(), sizeof(double) * 2 * in->h.masks.size());
+  if (masks && !in->h.masks.empty())
+    std::memcpy(masks, in->h.masks.data(), sizeof(double) * 2 * in->h.masks.size());
   return 0;
 }
 

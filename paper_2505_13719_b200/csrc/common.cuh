@@ -105,6 +105,10 @@ struct DevPairs {
   const double2* twid = nullptr;  // FftPlan forward twiddles (nc - 1)
   double2* F = nullptr;           // spectrum cache [kSMax][m]
   double2* G = nullptr;           // adjoint partials [kSMax][L][nc]
+  // Gaussian-measurement phase retrieval: the measurement
+  // vectors as an m x 2n row-major real matrix [Re a_i | Im a_i]; L is then the
+  // number of split-K parts of the adjoint (summed by pr_combine), nc = n
+  const double* gA = nullptr;
 };
 
 // Solver configuration (mirrors cuhallar_config / SolverConfig).

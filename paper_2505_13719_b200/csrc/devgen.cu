@@ -322,9 +322,41 @@ __global__ void sell_gather_k(const double* __restrict__ src, const uint32_t* __
   dst[t] = e != 0xffffffffu ? src[e] : 0.0;
 }
 
+// Gaussian measurement vectors: a_ij = (z1 + i z2) / sqrt(2), (z1, z2) by
+// Box-Muller from two uniforms of a counter hash of (seed, i, j); stored as the
+// m x 2n row-major [Re a_i | Im a_i] (device math: not the host RNG stream)
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+  z += 0x9e3779b97f4a7c15ULL;
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+  return z ^ (z >> 31);
+}
+__global__ void gauss_fill_k(double* __restrict__ A, int64_t m, int64_t n, uint64_t seed) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= m * n) return;
+  const int64_t i = t / n, j = t % n;
+  const uint64_t h1 = mix64(seed ^ mix64(uint64_t(t)));
+  const uint64_t h2 = mix64(h1);
+  const double u1 = (double((h1 >> 11) + 1)) * 0x1.0p-53;  // (0, 1]
+  const double u2 = double(h2 >> 11) * 0x1.0p-53;
+  const double r = sqrt(-2.0 * log(u1)) * 0.70710678118654752440;
+  double sn, cs;
+  sincospi(2.0 * u2, &sn, &cs);
+  A[i * 2 * n + j] = r * cs;
+  A[i * 2 * n + n + j] = r * sn;
+}
+
 }  // namespace
 
 // ------------------------------------------------------------------ API ---
+double* gauss_fill_device(int64_t m, int64_t n, uint64_t seed, cudaStream_t st) {
+  double* A = nullptr;
+  ck(cudaMalloc(&A, sizeof(double) * 2 * m * n), "gauss alloc");
+  gauss_fill_k<<<blocks(m * n), 256, 0, st>>>(A, m, n, seed);
+  ck(cudaGetLastError(), "gauss_fill");
+  ck(cudaStreamSynchronize(st), "gauss_fill");
+  return A;
+}
 int64_t sell_slots_device(int64_t n, const int64_t* up_ptr, const int64_t* lo_ptr, DevSell* out,
                           cudaStream_t st) {
   const int64_t nsl = (n + 31) / 32;

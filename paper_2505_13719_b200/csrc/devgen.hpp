@@ -69,4 +69,7 @@ void sell_fill_device(int64_t n, const int64_t* up_ptr, const int64_t* lo_ptr, c
 void sell_gather(const double* src_edge_order, const uint32_t* eid, int64_t slots, double* dst,
                  cudaStream_t st);
 
+// Gaussian phase retrieval: the m x 2n row-major [Re a_i | Im a_i] (caller frees)
+double* gauss_fill_device(int64_t m, int64_t n, uint64_t seed, cudaStream_t st);
+
 }  // namespace hallar_dev

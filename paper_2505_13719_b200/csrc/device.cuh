@@ -167,6 +167,23 @@ __device__ __forceinline__ void cpa4(void* d, const void* s) {
 __device__ __forceinline__ void cpa8(void* d, const void* s) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(d)), "l"(s) : "memory");
 }
+// the same copies with an L2 evict-first hint: streamed once per pass, they
+// must not push the gathered factor rows out of L2
+__device__ __forceinline__ unsigned long long l2_evict_first() {
+  unsigned long long pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ void cpa4s(void* d, const void* s, unsigned long long pol) {
+  asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 4, %2;" ::"r"(smem_u32(d)), "l"(s),
+               "l"(pol)
+               : "memory");
+}
+__device__ __forceinline__ void cpa8s(void* d, const void* s, unsigned long long pol) {
+  asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 8, %2;" ::"r"(smem_u32(d)), "l"(s),
+               "l"(pol)
+               : "memory");
+}
 __device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cpa_wait_group1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
 __device__ __forceinline__ void cpa_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
@@ -578,6 +595,201 @@ __device__ __forceinline__ void row_pass_sell(Ctx& c, const Params& P, const UA&
   __syncthreads();
 }
 
+// mbarrier + 1-D bulk copy (TMA) helpers
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_inval(unsigned long long* bar) {
+  asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, unsigned bytes,
+                                            unsigned long long* bar, unsigned long long pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
+      "[%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
+
+// Pipelined SELL engine: entry v of a slice's 32 rows is 32 consecutive
+// slots, so a batch of B entries of every stream (column index, multiplier,
+// right-hand side) is one contiguous block per stream.  Lane 0 of each warp
+// streams the NEXT batch's blocks into a shared-memory stage with 1-D bulk
+// copies (TMA, L2 evict-first, completion on a per-warp mbarrier) while the
+// warp gathers and folds the current batch: per batch only the gathers of
+// factor rows sit on the critical path (the passes are latency-bound at 16
+// warps per SM), and the streams cost no per-lane load instructions.  Same
+// fold as row_pass_sell, so results are bit-identical.
+template <int S, bool FIXED, bool HB, class UA, class Epi>
+__device__ __forceinline__ void row_pass_sell_async(Ctx& c, const Params& P, const UA& U,
+                                                    const double* __restrict__ Ps, double beta,
+                                                    double alpha, const double* cs, bool zero_init,
+                                                    double (&sums)[3], Epi& epi) {
+  static_assert(S >= 1 && S <= 4, "SELL engine: ranks 1..4");
+  constexpr int B = HB ? 4 : 8;  // per warp and stage: B x 32 x (4 + 8 [+ 8]) bytes
+  constexpr int kStageInts = B * 32;
+  static_assert((HB ? 5 : 3) * B * kThreads + 2 * kWarps <= kPassScratch,
+                "SELL stages exceed the pass scratch");
+  const DevPairs& I = P.I;
+  const int lane = c.lane, warp = c.warp;
+  // scratch: [warp][stage] col blocks (int32), p blocks, b blocks, then the barriers
+  int32_t* const colW = reinterpret_cast<int32_t*>(c.tw) + warp * 2 * kStageInts;
+  double* const pW = c.tw + B * kThreads + warp * 2 * kStageInts;
+  double* const bW = c.tw + 3 * B * kThreads + warp * 2 * kStageInts;
+  unsigned long long* const bar =
+      reinterpret_cast<unsigned long long*>(c.tw + (HB ? 5 : 3) * B * kThreads) + warp * 2;
+  double csr[S];
+#pragma unroll
+  for (int k = 0; k < S; ++k) csr[k] = cs ? cs[k] : 0.0;
+  const int64_t sl1 = (c.rh + 31) >> 5;
+  struct Sl {
+    int64_t a, s_beg;
+    int L, nv, nlo;
+    bool mine;
+  };
+  auto slice = [&](int64_t sl) {
+    Sl x;
+    x.a = (sl << 5) + lane;
+    x.mine = x.a >= c.rl && x.a < c.rh;
+    x.s_beg = __ldg(I.s_off + sl);
+    x.L = (int)((__ldg(I.s_off + sl + 1) - x.s_beg) >> 5);
+    x.nv = x.mine ? __ldg(I.s_nv + x.a) : 0;
+    x.nlo = x.mine ? __ldg(I.s_nlo + x.a) : 0;
+    return x;
+  };
+  const unsigned long long pol = l2_evict_first();
+  auto issue = [&](int st, const Sl& x, int v0) {  // lane 0 only
+    const int ne = min(B, x.L - v0) * 32;
+    const int64_t g = x.s_beg + (int64_t)v0 * 32;
+    mbar_expect_tx(bar + st, (unsigned)ne * (HB ? 20u : 12u));
+    tma_load_1d(colW + st * kStageInts, I.s_col + g, ne * 4, bar + st, pol);
+    tma_load_1d(pW + st * kStageInts, Ps + g, ne * 8, bar + st, pol);
+    if (HB) tma_load_1d(bW + st * kStageInts, I.s_b + g, ne * 8, bar + st, pol);
+  };
+  int64_t sl = (c.rl >> 5) + warp;
+  if (sl < sl1) {
+    if (lane == 0) {
+      mbar_init(bar, 1);
+      mbar_init(bar + 1, 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+    Sl X = slice(sl);
+    int st = 0;
+    unsigned phase = 0;  // bit st: parity of stage st's next completion
+    if (lane == 0 && X.L > 0) issue(0, X, 0);
+    while (true) {
+      double ua[S], acc[S];
+      if (X.mine) {
+        sell_row<S>(U, X.a, ua);
+      } else {
+#pragma unroll
+        for (int k = 0; k < S; ++k) ua[k] = 0.0;
+      }
+#pragma unroll
+      for (int k = 0; k < S; ++k) {
+        acc[k] = 0.0;
+        if (!zero_init) {
+          acc[k] = alpha * ua[k];
+          if (cs) acc[k] = acc[k] - csr[k];
+        }
+      }
+      const int64_t sln = sl + kWarps;
+      const bool have_next = sln < sl1;
+      Sl XN{};
+      if (have_next) XN = slice(sln);
+#pragma unroll 1
+      for (int v0 = 0; v0 < X.L; v0 += B) {
+        // the next batch (this slice, or the next slice's first) in flight
+        if (lane == 0) {
+          if (v0 + B < X.L)
+            issue(st ^ 1, X, v0 + B);
+          else if (have_next && XN.L > 0)
+            issue(st ^ 1, XN, 0);
+        }
+        mbar_wait(bar + st, (phase >> st) & 1u);
+        phase ^= 1u << st;
+        int32_t bc[B];
+        double pk[B], bk[B];
+#pragma unroll
+        for (int u = 0; u < B; ++u) {
+          const bool ok = v0 + u < X.nv;
+          bc[u] = ok ? colW[st * kStageInts + u * 32 + lane] : 0;
+          pk[u] = ok ? pW[st * kStageInts + u * 32 + lane] : 0.0;
+          bk[u] = (ok && HB) ? bW[st * kStageInts + u * 32 + lane] : 0.0;
+        }
+        __syncwarp();  // stage st is refilled by the next-but-one issue
+        double ub[B][S];
+#pragma unroll
+        for (int u = 0; u < B; ++u) {
+          if (v0 + u < X.nv) {
+            sell_row<S>(U, bc[u], ub[u]);
+          } else {
+#pragma unroll
+            for (int k = 0; k < S; ++k) ub[u][k] = 0.0;
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < B; ++u) {
+          const int v = v0 + u;
+          if (v >= X.nv) break;
+          const bool upper = v >= X.nlo;
+          double w;
+          if (FIXED) {
+            w = 0.5 * pk[u];
+          } else {
+            double d = 0.0;
+#pragma unroll
+            for (int k = 0; k < S; ++k) {
+              const double tt = ua[k] * ub[u][k];
+              d = (k == 0) ? tt : d + tt;
+            }
+            const double rr = d - bk[u];
+            const double q = pk[u] + beta * rr;
+            w = 0.5 * q;
+            if (upper) {
+              sums[0] = sums[0] + pk[u] * rr;
+              sums[1] = sums[1] + rr * rr;
+              sums[2] = sums[2] + q * (rr + bk[u]);
+            }
+          }
+          // skipped terms (w == 0, instances.cpp:47): x + (-0.0) == x exactly
+#pragma unroll
+          for (int k = 0; k < S; ++k) acc[k] = acc[k] + ((w != 0.0) ? w * ub[u][k] : -0.0);
+        }
+        st ^= 1;
+      }
+      if (X.mine) {
+#pragma unroll
+        for (int k = 0; k < S; ++k) epi(X.a, k, acc[k], ua[k]);
+      }
+      if (!have_next) break;
+      if (X.L == 0 && lane == 0 && XN.L > 0) issue(st, XN, 0);  // nothing was prefetched
+      sl = sln;
+      X = XN;
+    }
+    __syncwarp();
+    if (lane == 0) {
+      mbar_inval(bar);
+      mbar_inval(bar + 1);
+    }
+  }
+  __syncthreads();
+}
+
 // SELL-order copy of a multiplier given its edge-order array (null: none)
 __device__ __forceinline__ const double* sell_of(const Params& P, const double* up) {
   if (!P.I.s_col) return nullptr;
@@ -612,7 +824,14 @@ __device__ __forceinline__ void row_pass_t(Ctx& c, const Params& P, const UA& U,
     if (c.rh - c.rl >= kRtMinRows) {
       const double* Ps = sell_of(P, Pup);
       if (Ps && sell_aligned<S>(U.base())) {
-        row_pass_sell<S, FIXED>(c, P, U, Ps, beta, alpha, cs, zero_init, sums, epi);
+        if constexpr (!FIXED) {
+          if (I.s_b)
+            row_pass_sell_async<S, false, true>(c, P, U, Ps, beta, alpha, cs, zero_init, sums, epi);
+          else
+            row_pass_sell_async<S, false, false>(c, P, U, Ps, beta, alpha, cs, zero_init, sums, epi);
+        } else {
+          row_pass_sell_async<S, true, false>(c, P, U, Ps, beta, alpha, cs, zero_init, sums, epi);
+        }
         return;
       }
       // fixed q: cp.async-staged stream (measured 27% faster at H(23,2), s = 1);
@@ -973,6 +1192,22 @@ struct RowSrc {
     const double z = XT[o] - GT[o] / L;
     return scale ? z / nrm : z;
   }
+  // row b (S values), vector loads: same values as at(b * S + k)
+  template <int S>
+  __device__ __forceinline__ void row(int64_t b, double (&o)[S]) const {
+    if (U) {
+      sell_row<S>(UPlain{U}, b, o);
+      return;
+    }
+    double x[S], g[S];
+    sell_row<S>(UPlain{XT}, b, x);
+    sell_row<S>(UPlain{GT}, b, g);
+#pragma unroll
+    for (int k = 0; k < S; ++k) {
+      const double z = x[k] - g[k] / L;
+      o[k] = scale ? z / nrm : z;
+    }
+  }
 };
 
 template <int S>
@@ -999,7 +1234,17 @@ __device__ __forceinline__ void map_pass_src(Ctx& c, const Params& P, const RowS
 #pragma unroll
     for (int u = 0; u < kUnroll; ++u) {
       double acc = 0.0;
-      if (S > 0) {
+      if constexpr (S > 0 && S <= 4) {
+        // both rows with the widest aligned vector loads (sell_row)
+        double ri[S], rj[S];
+        src.row<S>(ii[u], ri);
+        src.row<S>(jj[u], rj);
+#pragma unroll
+        for (int cc = 0; cc < S; ++cc) {
+          const double t = ri[cc] * rj[cc];
+          acc = (cc == 0) ? t : acc + t;
+        }
+      } else if (S > 0) {
 #pragma unroll
         for (int cc = 0; cc < (S > 0 ? S : 1); ++cc) {
           const double t = src.at(ii[u] * s + cc) * src.at(jj[u] * s + cc);
@@ -1538,6 +1783,24 @@ __device__ __noinline__ bool aipp_dev(Ctx& c, const Params& P, Roles& R, int s, 
       FistaOut fo;
       if (!fista_dev<S>(c, P, R, s, lambda, fmax(1.0, M_bar / 2.0), fo)) return false;
       out.fista_iters += fo.iters;
+      if (P.cfg.trace >= 2 && P.trace && c.t.rank == 0 && threadIdx.x == 0) {
+        // debug (cfg.trace >= 2): one event per fista() call, kind 9 (L0 in
+        // eps_inner, status in rank, iterations in outer_iter, final L in gap,
+        // psi_y in theta, the prox step lambda in fw_alpha)
+        const int i = *P.trace_count;
+        if (i < P.trace_cap) {
+          TraceEv ev{};
+          ev.kind = 9;
+          ev.eps_inner = fmax(1.0, M_bar / 2.0);
+          ev.rank = fo.status;
+          ev.outer_iter = fo.iters;
+          ev.gap = fo.L;
+          ev.theta = fo.status == 2 ? 0.0 : fo.psi_y;
+          ev.fw_alpha = lambda;
+          P.trace[i] = ev;
+        }
+        *P.trace_count = i + 1;
+      }
       if (fo.status == 0) {
         const double step_sq = fo.dist0;
         g_W = (fo.psi_y - 0.5 * step_sq) / lambda;

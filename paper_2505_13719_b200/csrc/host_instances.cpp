@@ -471,4 +471,29 @@ HostInst make_phaseret(int64_t n, int L, uint64_t seed, double tau_slack) {
   return h;
 }
 
+HostInst make_gauss_pr(int64_t n, int64_t m, int parts, uint64_t seed, double tau_slack) {
+  if (n < 1 || m < 1) throw InputError("gauss_pr: n and m must be >= 1");
+  if (!(tau_slack >= 1.0)) throw InputError("gauss_pr: tau_slack must be >= 1");
+  HostInst h;
+  h.family = 2;
+  h.nc = n;
+  h.L = parts;
+  h.n = 2 * n;
+  h.m = m;
+  Xoshiro g(seed);
+  h.hidden_x.resize(n);
+  for (int64_t j = 0; j < n; ++j) {
+    const double im = g.normal();
+    const double re = g.normal();
+    h.hidden_x[j] = {re / std::sqrt(2.0), im / std::sqrt(2.0)};
+  }
+  const double sx = eigen_sum(n, [&](int64_t j) {
+    const auto& z = h.hidden_x[j];
+    return z.real() * z.real() + z.imag() * z.imag();
+  });
+  h.tau = tau_slack * sx;
+  h.norm_C1 = double(2 * n);
+  return h;
+}
+
 }  // namespace hallar_host

@@ -85,6 +85,10 @@ struct McPrefix {
 McPrefix matcomp_prefix(int64_t n1, int64_t n2, int r, uint64_t seed, bool offset, double tau_safety,
                         int64_t paper_draws);
 HostInst make_phaseret(int64_t n, int L, uint64_t seed, double tau_slack);
+// Gaussian-measurement phase retrieval (not in the
+// reference): the signal x from Rng(seed) as make_phaseret draws it; the
+// measurement vectors are generated on the device (devgen.cu gauss_fill).
+HostInst make_gauss_pr(int64_t n, int64_t m, int parts, uint64_t seed, double tau_slack);
 
 // Eigen LinearVectorized redux order (SSE2, 2 accumulators of 2 lanes).
 double eigen_order_sum_sq(const double* x, int64_t n);

@@ -85,6 +85,168 @@ __device__ __forceinline__ void fft_smem(double2* X, int nc, int logn,
   else if (logn - st == 1) fft_pass<1, INV>(X, nc, st, tw);
 }
 
+// (pr_map_value is needed by the Gaussian variant below)
+__device__ __forceinline__ double pr_map_value(const DevPairs& I, int64_t k, int s);
+
+// ------------------------------------------ Gaussian-measurement variant ---
+// SURVEY §8(f) row 3 (BASELINE configs[2]; not in the reference: parity is
+// the dense oracle of oracle/src/families.cpp gauss_pr_instance, unpinned
+// against the reference).  Constraint i is |a_i^* u|^2 summed over columns;
+// with A' = [Re A | Im A] (m x 2n row-major, HBM) both operator halves are
+// real GEMMs with an 8-wide right-hand side, run on the FP64 tensor cores
+// (DMMA, mma.sync m8n8k4 f64):
+//   forward  Y = A' W,   W = [U1 | U2] (2n x 8): U1 = [Re u_c; Im u_c],
+//            U2 = [Im u_c; -Re u_c]  ->  F[c][i] = (Y[i][c], Y[i][4 + c])
+//   adjoint  D1 = A'[:, :n]^T V, D2 = A'[:, n:]^T V, V = [Re w | Im w] (m x 8),
+//            w_ic = q_i F[c][i]  ->  z_c = (D1[:, c] - D2[:, 4+c]) + i (D1[:, 4+c] + D2[:, c])
+// Each streams A' from HBM once per call (the roofline: 16 m n bytes); the
+// right-hand side is staged per CTA in shared-memory chunks.  Columns go in
+// groups of four.  The adjoint splits the m measurements into I.L parts
+// (partials G[c][part][j], summed in part order by pr_combine).
+__device__ __forceinline__ void dmma884(double (&d)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(d[0]), "+d"(d[1])
+               : "d"(a), "d"(b));
+}
+constexpr int kGprChunk = 512;  // rows of the staged right-hand side (x 8 doubles)
+
+template <class UA>
+__device__ __noinline__ void gpr_forward(const Params& P, int rank, int size, double* Ws, const UA U,
+                                         int s) {
+  const DevPairs& I = P.I;
+  const int64_t n = I.nc, n2 = 2 * I.nc, m = I.m;
+  const double* __restrict__ A = I.gA;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int ng = (s + 3) / 4;
+  const int64_t nblk = (m + 8 * kWarps - 1) / (8 * kWarps);
+  for (int64_t item = rank; item < nblk * ng; item += size) {
+    const int64_t blk = item / ng;
+    const int c0 = (int)(item % ng) * 4, sc = min(4, s - c0);
+    const int64_t row = blk * 8 * kWarps + warp * 8 + (lane >> 2);
+    const double* ar = A + (row < m ? row : m - 1) * n2 + (lane & 3);
+    double acc[2] = {0.0, 0.0}, acc2[2] = {0.0, 0.0};
+    for (int64_t k0 = 0; k0 < n2; k0 += kGprChunk) {
+      __syncthreads();
+      for (int idx = threadIdx.x; idx < kGprChunk * 8; idx += kThreads) {
+        const int kk = idx >> 3, cc = idx & 7, cl = cc & 3;
+        const int64_t k = k0 + kk;
+        double v = 0.0;
+        if (k < n2 && cl < sc) {
+          const int col = c0 + cl;
+          if (cc < 4)
+            v = U(k * s + col);
+          else
+            v = k < n ? U((n + k) * s + col) : -U((k - n) * s + col);
+        }
+        Ws[idx] = v;
+      }
+      __syncthreads();
+      const int kmax = (int)min((int64_t)kGprChunk, n2 - k0);
+#pragma unroll 4
+      for (int kk = 0; kk < kmax; kk += 8) {
+        const bool ok0 = row < m && k0 + kk + (lane & 3) < n2;
+        const bool ok1 = row < m && k0 + kk + 4 + (lane & 3) < n2;
+        const double a0 = ok0 ? __ldcs(ar + k0 + kk) : 0.0;
+        const double a1 = ok1 ? __ldcs(ar + k0 + kk + 4) : 0.0;
+        dmma884(acc, a0, Ws[(kk + (lane & 3)) * 8 + (lane >> 2)]);
+        dmma884(acc2, a1, Ws[(kk + 4 + (lane & 3)) * 8 + (lane >> 2)]);
+      }
+    }
+    // lane holds Y[row][2 tq + e], tq = lane & 3: tq 0/1 real parts of columns
+    // 2tq + e, tq 2/3 the matching imaginary parts (lane + 2)
+    const double y0 = acc[0] + acc2[0], y1 = acc[1] + acc2[1];
+    const double i0 = __shfl_down_sync(0xffffffffu, y0, 2);
+    const double i1 = __shfl_down_sync(0xffffffffu, y1, 2);
+    const int tq = lane & 3;
+    if (tq < 2 && row < m) {
+      const int c = 2 * tq;
+      if (c < sc) I.F[(int64_t)(c0 + c) * m + row] = make_double2(y0, i0);
+      if (c + 1 < sc) I.F[(int64_t)(c0 + c + 1) * m + row] = make_double2(y1, i1);
+    }
+  }
+  __syncthreads();
+}
+
+template <bool FIXED>
+__device__ __noinline__ void gpr_inverse(const Params& P, int rank, int size, double* Ws, int s,
+                                         const double* __restrict__ qv, const double* __restrict__ pv,
+                                         double beta, double* sums) {
+  const DevPairs& I = P.I;
+  const int64_t n = I.nc, n2 = 2 * I.nc, m = I.m;
+  const int parts = I.L;
+  const double* __restrict__ A = I.gA;
+  const double* __restrict__ bv = I.b_up;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int ng = (s + 3) / 4;
+  const int64_t ntile = (n + 7) / 8, njg = (ntile + kWarps - 1) / kWarps;
+  const int64_t items = (int64_t)parts * njg * ng;
+  for (int64_t item = rank; item < items; item += size) {
+    const int part = (int)(item / (njg * ng));
+    const int64_t jg = (item / ng) % njg;
+    const int c0 = (int)(item % ng) * 4, sc = min(4, s - c0);
+    const int64_t i_lo = m * part / parts, i_hi = m * (part + 1) / parts;
+    const int64_t j0 = (jg * kWarps + warp) * 8;
+    const int64_t jr = j0 + (lane >> 2);
+    const bool jok = jr < n;
+    const bool do_sums = !FIXED && jg == 0 && c0 == 0;
+    double d1[2] = {0.0, 0.0}, d2[2] = {0.0, 0.0};
+    for (int64_t ib = i_lo; ib < i_hi; ib += kGprChunk) {
+      __syncthreads();
+      // V chunk: V[ii][cc] = Re / Im of w_ic = q_i F[c][i]
+      for (int idx = threadIdx.x; idx < kGprChunk * 8; idx += kThreads) {
+        const int ii = idx >> 3, cc = idx & 7, cl = cc & 3;
+        const int64_t i = ib + ii;
+        double v = 0.0;
+        if (i < i_hi && cl < sc) {
+          double q;
+          if (FIXED) {
+            q = qv[i];
+          } else {
+            const double d = pr_map_value(I, i, s);
+            const double bb = bv ? bv[i] : 0.0;
+            const double r = d - bb;
+            const double pk = pv[i];
+            q = pk + beta * r;
+            if (do_sums && cc == 0) {
+              sums[0] = sums[0] + pk * r;
+              sums[1] = sums[1] + r * r;
+              sums[2] = sums[2] + q * (r + bb);
+            }
+          }
+          const double2 f = I.F[(int64_t)(c0 + cl) * m + i];
+          v = cc < 4 ? f.x * q : f.y * q;
+        }
+        Ws[idx] = v;
+      }
+      __syncthreads();
+      if (j0 < n) {
+        const int imax = (int)min((int64_t)kGprChunk, i_hi - ib);
+#pragma unroll 4
+        for (int ii = 0; ii < imax; ii += 4) {
+          const int64_t i = ib + ii + (lane & 3);
+          const bool ok = jok && i < i_hi;
+          const double a1 = ok ? __ldcs(A + i * n2 + jr) : 0.0;
+          const double a2 = ok ? __ldcs(A + i * n2 + n + jr) : 0.0;
+          const double b = Ws[(ii + (lane & 3)) * 8 + (lane >> 2)];
+          dmma884(d1, a1, b);
+          dmma884(d2, a2, b);
+        }
+      }
+    }
+    // lane holds D1/D2[jr][2 tq + e]; the imaginary-weight columns 4 + c sit in lane + 2
+    const double e1a = __shfl_down_sync(0xffffffffu, d1[0], 2), e1b = __shfl_down_sync(0xffffffffu, d1[1], 2);
+    const double e2a = __shfl_down_sync(0xffffffffu, d2[0], 2), e2b = __shfl_down_sync(0xffffffffu, d2[1], 2);
+    const int tq = lane & 3;
+    if (tq < 2 && jok) {
+      const int c = 2 * tq;
+      double2* G = I.G + ((int64_t)(c0 + c) * parts + part) * n + jr;
+      if (c < sc) G[0] = make_double2(d1[0] - e2a, e1a + d2[0]);
+      if (c + 1 < sc) G[(int64_t)parts * n] = make_double2(d1[1] - e2b, e1b + d2[1]);
+    }
+  }
+  __syncthreads();
+}
+
 // Forward tasks: F[c*m + l*nc + k] = FFT(d_l .* u_c)_k for c < s, l < L.
 // U(o) returns factor element o = row * s + column.  Caller team-syncs
 // before (U complete) and after (F complete).
@@ -92,6 +254,10 @@ template <class UA>
 __device__ __noinline__ void pr_forward(const Params& P, int rank, int size, double2* X, const UA U,
                                         int s) {
   const DevPairs& I = P.I;
+  if (I.gA) {
+    gpr_forward(P, rank, size, reinterpret_cast<double*>(X), U, s);
+    return;
+  }
   const int nc = (int)I.nc, L = I.L, logn = I.lognc;
   for (int task = rank; task < s * L; task += size) {
     const int col = task / L, l = task % L;
@@ -132,6 +298,10 @@ __device__ __noinline__ void pr_inverse(const Params& P, int rank, int size, dou
                                         const double* __restrict__ pv, double beta,
                                         double* sums) {
   const DevPairs& I = P.I;
+  if (I.gA) {
+    gpr_inverse<FIXED>(P, rank, size, reinterpret_cast<double*>(X), s, qv, pv, beta, sums);
+    return;
+  }
   const int nc = (int)I.nc, L = I.L, logn = I.lognc;
   const double* __restrict__ bv = I.b_up;
   for (int task = rank; task < s * L; task += size) {

@@ -243,11 +243,49 @@ __device__ __forceinline__ void lz_dot_small(Ctx& c, const Params& P, int k, con
   team_reduce_smem(c.t, c.rs, k);
 }
 
+// Large instances: h[i] = V_i . w' over this CTA's rows with a thread per
+// row, so basis vector i is read coalesced (consecutive threads, consecutive
+// rows); the basis is taken 8 vectors at a time (8 partial sums per thread in
+// registers, w re-read per group), optionally after w' = w - V_k hs (same
+// thread, same rows: lz_row_dot order).  Partials are reduced warp -> CTA ->
+// team in a fixed tree (deterministic).
+template <bool SUB>
+__device__ __forceinline__ void lz_dot_rows(Ctx& c, const Params& P, int k, double* w,
+                                            const double* hs) {
+  if (SUB)
+    for (int64_t a = c.rl + threadIdx.x; a < c.rh; a += kThreads) w[a] = w[a] - lz_row_dot(c, P, k, a, hs);
+  for (int g = 0; g < k; g += 8) {
+    const double* v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = slot_ptr(P, c.col[g + u < k ? g + u : g]);
+    double acc[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) acc[u] = 0.0;
+    for (int64_t a = c.rl + threadIdx.x; a < c.rh; a += kThreads) {
+      const double wa = w[a];
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (g + u < k) acc[u] = acc[u] + v[u][a] * wa;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (g + u < k) {
+        const double x = warp_sum(acc[u]);
+        if (c.lane == 0) c.rs.part[c.warp * kRedK + g + u] = x;
+      }
+  }
+  team_reduce_smem(c.t, c.rs, k);
+}
+
 __device__ __forceinline__ void lz_dot(Ctx& c, const Params& P, int k, const double* w) {
   const int lane = c.lane;
   const int64_t rl = c.rl, rh = c.rh;
   if (rh - rl <= 32) {
     lz_dot_small(c, P, k, w, rh - rl);
+    return;
+  }
+  if (rh - rl >= kRtMinRows) {
+    lz_dot_rows<false>(c, P, k, const_cast<double*>(w), nullptr);
     return;
   }
   const double* vi = slot_ptr(P, c.col[lane < k ? lane : 0]);
@@ -303,6 +341,10 @@ __device__ __forceinline__ void lz_sub(Ctx& c, const Params& P, int k, double* w
       }
       team_sum<2>(c.t, c.rs, v);
     }
+    return;
+  }
+  if (dot_after && rh - rl >= kRtMinRows) {
+    lz_dot_rows<true>(c, P, k, w, h);
     return;
   }
   const double* vi = slot_ptr(P, c.col[lane < k ? lane : 0]);

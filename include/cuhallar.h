@@ -222,6 +222,20 @@ int cuhallar_solve(cuhallar_instance* inst, const cuhallar_config* cfg, const do
 int cuhallar_solve_sharded(cuhallar_instance* const* insts, int world, const cuhallar_config* cfg,
                            const double* U0_host, int s0, const double* p0_host,
                            cuhallar_report* rep, cuhallar_solution** sol);
+
+/* The same row-sharded solve with one process per GPU (torchrun): every rank
+ * builds the instance on its own device, exports its rendezvous / partial-sum /
+ * factor-arena allocations as CUDA IPC handles, the ranks exchange the handles
+ * (any host-side collective) and call cuhallar_solve_rank concurrently.  Rows
+ * and constraints are owned by rank as in cuhallar_solve_sharded; reductions
+ * join per-rank partials in rank order, so every rank reports the same
+ * scalars.  The solution's U is complete on every rank (replicated factor
+ * arena); its p holds this rank's constraints (first index in its rows). */
+typedef struct { unsigned char bytes[512]; } cuhallar_shard_handle;
+int cuhallar_shard_export(cuhallar_instance* inst, int team_ctas, cuhallar_shard_handle* out);
+int cuhallar_solve_rank(cuhallar_instance* inst, int world, int rank, const cuhallar_shard_handle* peers,
+                        const cuhallar_config* cfg, const double* U0_or_null, int s0,
+                        const double* p0_or_null, cuhallar_report* rep, cuhallar_solution** sol);
 /* SolveReport::U (n x rank, column-major) and SolveReport::dual.p (length m) */
 int cuhallar_solution_get_U(const cuhallar_solution* sol, double* U_host);
 int cuhallar_solution_get_p(const cuhallar_solution* sol, double* p_host);

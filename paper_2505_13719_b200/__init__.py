@@ -9,5 +9,6 @@ from .api import (  # noqa: F401
     CudaError, GaussPrSpec, Graph, InputError, McSpec, NumericalError, PrSpec, SdpInstance, SolveReport,
     SolverConfig, TraceEvent, build_theta_instance, gen_gauss_phase_retrieval, gen_matrix_completion, gen_phase_retrieval,
     graph_from_edges, load_graph, make_cycle, make_hypercube, make_petersen,
-    matcomp_constraint_count, matcomp_from_samples, solve, solve_sharded, version, LIB_PATH,
+    matcomp_constraint_count, matcomp_from_samples, shard_export, solve, solve_rank, solve_sharded, version,
+    LIB_PATH,
 )

@@ -583,10 +583,12 @@ def solve(inst: SdpInstance, cfg: SolverConfig = None, U0=None, p0=None,
     sol = C.c_void_p()
     events = []
 
-    def _cb(ev, _u):
+    def _cb(ev, _u):  # called while the solve runs (trace.hpp sink semantics)
         e = ev.contents
-        events.append(TraceEvent(TRACE_KIND[e.kind], e.outer_iter, e.beta, e.eps_inner, e.gap, e.theta,
-                                 e.rank, e.al_value, e.fw_alpha, e.rel_pfeas, e.rel_gap, e.rel_dfeas))
+        te = TraceEvent(TRACE_KIND.get(e.kind, str(e.kind)), e.outer_iter, e.beta, e.eps_inner, e.gap,
+                        e.theta, e.rank, e.al_value, e.fw_alpha, e.rel_pfeas, e.rel_gap, e.rel_dfeas)
+        events.append(te)
+        sink(te)
 
     cb = _TRACE_FN(_cb) if sink is not None else _TRACE_FN()
     U0p, s0, p0p, _keep = _start_args(inst, U0, p0)
@@ -595,8 +597,6 @@ def solve(inst: SdpInstance, cfg: SolverConfig = None, U0=None, p0=None,
     _check(rc)
     r = _report(inst, rep, sol, fetch)
     if sink is not None:
-        for e in events:
-            sink(e)
         r.trace = events
     return r
 
@@ -624,6 +624,34 @@ def solve_sharded(insts, cfg: SolverConfig = None, U0=None, p0=None, fetch: bool
     _check(_lib.cuhallar_solve_sharded(arr, C.c_int(len(insts)), C.byref(cc), U0p, C.c_int(s0), p0p,
                                        C.byref(rep), C.byref(sol)))
     return _report(insts[0], rep, sol, fetch)
+
+
+class ShardHandle(C.Structure):
+    _fields_ = [("bytes", C.c_ubyte * 512)]
+
+
+def shard_export(inst: SdpInstance, team_ctas: int = 0) -> bytes:
+    """This rank's IPC handles for the one-process-per-GPU sharded solve."""
+    h = ShardHandle()
+    _check(_lib.cuhallar_shard_export(inst._h, C.c_int(team_ctas), C.byref(h)))
+    return bytes(h.bytes)
+
+
+def solve_rank(inst: SdpInstance, world: int, rank: int, handles, cfg: SolverConfig = None,
+               fetch: bool = False) -> SolveReport:
+    """Row-sharded solve, one process per GPU (torchrun): ``handles[q]`` is rank q's
+    ``shard_export`` blob (exchanged by any collective); every rank calls this
+    concurrently and gets the same report."""
+    cfg = cfg or SolverConfig()
+    cc = cfg._c()
+    arr = (ShardHandle * world)()
+    for q, hb in enumerate(handles):
+        C.memmove(arr[q].bytes, hb, 512)
+    rep = CReport()
+    sol = C.c_void_p()
+    _check(_lib.cuhallar_solve_rank(inst._h, C.c_int(world), C.c_int(rank), arr, C.byref(cc), None, C.c_int(0),
+                                    None, C.byref(rep), C.byref(sol)))
+    return _report(inst, rep, sol, fetch)
 
 
 def _report(inst, rep, sol, fetch) -> SolveReport:

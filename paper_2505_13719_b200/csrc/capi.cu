@@ -11,6 +11,7 @@
 #include <cstring>
 #include <memory>
 #include <mutex>
+#include <functional>
 #include <atomic>
 #include <thread>
 #include <string>
@@ -426,7 +427,7 @@ void ensure_workspace(cuhallar_instance* in, int grid, uint64_t seed, int block_
 
 Params base_params(cuhallar_instance* in, const cuhallar_config* cfg);
 int launch(cuhallar_instance* in, Params& P, int grid, cudaStream_t st, SolveOut* so,
-           float* ms = nullptr);
+           float* ms = nullptr, const std::function<void()>& poll = nullptr);
 
 void upload_pr(cuhallar_instance* in);
 // Gaussian phase retrieval: A' generated on the device, the spectrum cache F
@@ -734,7 +735,7 @@ struct RefillService {
 
 // Launch the persistent kernel; returns the solver status and fills *so.
 int launch(cuhallar_instance* in, Params& P, int grid, cudaStream_t st, SolveOut* so,
-           float* ms) {
+           float* ms, const std::function<void()>& poll) {
   ck(cudaMemsetAsync(in->bar, 0, sizeof(unsigned long long), st), "memset bar");
   ck(cudaMemsetAsync(in->dso, 0, sizeof(SolveOut), st), "memset out");
   if (in->trace_count_host) *in->trace_count_host = 0;
@@ -762,6 +763,14 @@ int launch(cuhallar_instance* in, Params& P, int grid, cudaStream_t st, SolveOut
      "cooperative launch");
   if (ms) ck(cudaEventRecord(e1, st), "event");
   ck(cudaMemcpyAsync(so, in->dso, sizeof(SolveOut), cudaMemcpyDeviceToHost, st), "D2H out");
+  if (poll) {  // e.g. trace events delivered while the solve runs
+    cudaError_t q;
+    while ((q = cudaStreamQuery(st)) == cudaErrorNotReady) {
+      poll();
+      std::this_thread::sleep_for(std::chrono::milliseconds(2));
+    }
+    if (q != cudaSuccess) ck(q, "hallar_kernel");
+  }
   ck(cudaStreamSynchronize(st), "hallar_kernel");
   svc.reset();
   if (ms) {
@@ -1287,7 +1296,22 @@ int cuhallar_solve(cuhallar_instance* in, const cuhallar_config* cfg, const doub
     }
     SolveOut so{};
     float ms = 0.f;
-    const int stt = launch(in, P, grid, 0, &so, &ms);
+    // trace.hpp sinks see the events while the solve runs (the ring is mapped
+    // host memory; an event is complete once the count has moved past it)
+    int delivered = 0;
+    auto deliver = [&](bool all) {
+      if (!fn || !cfg->trace) return;
+      int cnt = std::min(static_cast<int>(*(volatile int*)in->trace_count_host), in->trace_cap);
+      if (!all) cnt = std::max(delivered, cnt - 1);
+      for (; delivered < cnt; ++delivered) {
+        const TraceEv& e = in->trace_host[delivered];
+        cuhallar_trace_event ev{e.kind, e.outer_iter, e.beta, e.eps_inner, e.gap, e.theta,
+                                e.rank, e.al_value, e.fw_alpha, e.rel_pfeas, e.rel_gap,
+                                e.rel_dfeas};
+        fn(&ev, user);
+      }
+    };
+    const int stt = launch(in, P, grid, 0, &so, &ms, [&] { deliver(false); });
     if (cfg->profile) {
       in->last_prof.assign(2 * kProfCats, 0);
       ck(cudaMemcpy(in->last_prof.data(), in->dprof, sizeof(unsigned long long) * 2 * kProfCats,
@@ -1296,16 +1320,8 @@ int cuhallar_solve(cuhallar_instance* in, const cuhallar_config* cfg, const doub
     }
     const double wall =
         std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();
-    if (fn && cfg->trace) {
-      const int cnt = std::min(*in->trace_count_host, in->trace_cap);
-      for (int i = 0; i < cnt; ++i) {
-        const TraceEv& e = in->trace_host[i];
-        cuhallar_trace_event ev{e.kind, e.outer_iter, e.beta, e.eps_inner, e.gap, e.theta,
-                                e.rank, e.al_value, e.fw_alpha, e.rel_pfeas, e.rel_gap,
-                                e.rel_dfeas};
-        fn(&ev, user);
-      }
-    }
+    deliver(true);
+    (void)stt;
     (void)n;
     return fill_report(in, so, ms, wall, rep, sol, {in});
   });
@@ -1512,6 +1528,110 @@ int cuhallar_solve_sharded(cuhallar_instance* const* insts, int world, const cuh
     const double wall =
         std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();
     return fill_report(R[0], so, ms, wall, rep, sol, R);
+  });
+}
+
+// ---- one process per GPU (torchrun): the same row-owner sharded solve with
+// the peers' rendezvous counters, partial slots and factor arenas mapped
+// through CUDA IPC handles instead of one process's peer pointers.
+int cuhallar_shard_export(cuhallar_instance* in, int team_ctas, cuhallar_shard_handle* out) {
+  return guard([&] {
+    DevGuard dg(in->device);
+    if (in->h.family == kPhaseret)
+      throw hh::InputError("sharded solve: phase retrieval does not shard (replicas only)");
+    std::lock_guard<std::mutex> lk(in->mu);
+    const int G = grid_size(team_ctas);
+    ensure_workspace(in, G, in->lz_seed == ~0ull ? 0 : in->lz_seed, 30);
+    if (!in->xbar) {
+      in->xbar = dalloc<unsigned long long>(1, &in->bytes);
+      in->xslots = dalloc<double>(size_t(2) * kMaxWorld * kRedK, &in->bytes);
+      in->xerr = dalloc<int>(1, &in->bytes);
+    }
+    std::memset(out, 0, sizeof(*out));
+    cudaIpcMemHandle_t h[3];
+    ck(cudaIpcGetMemHandle(&h[0], in->xbar), "ipc xbar");
+    ck(cudaIpcGetMemHandle(&h[1], in->xslots), "ipc xslots");
+    ck(cudaIpcGetMemHandle(&h[2], in->arena), "ipc arena");
+    static_assert(3 * sizeof(cudaIpcMemHandle_t) + 32 <= sizeof(out->bytes), "handle blob");
+    std::memcpy(out->bytes, h, sizeof(h));
+    int64_t meta[4] = {in->h.n, in->h.np, in->arena_len, G};
+    std::memcpy(out->bytes + sizeof(h), meta, sizeof(meta));
+    return 0;
+  });
+}
+
+int cuhallar_solve_rank(cuhallar_instance* in, int world, int rank, const cuhallar_shard_handle* peers,
+                        const cuhallar_config* cfg, const double* U0_host, int s0,
+                        const double* p0_host, cuhallar_report* rep, cuhallar_solution** sol) {
+  return guard([&] {
+    if (world < 1 || world > kMaxWorld) throw hh::InputError("sharded solve: world must lie in [1, 8]");
+    if (rank < 0 || rank >= world) throw hh::InputError("sharded solve: rank out of range");
+    validate_cfg(*cfg);
+    if (cfg->parity) throw hh::InputError("parity mode: single-GPU solve only");
+    DevGuard dg(in->device);
+    std::lock_guard<std::mutex> lk(in->mu);
+    if (!in->xbar) throw hh::InputError("sharded solve: cuhallar_shard_export first");
+    int64_t meta0[4];
+    std::memcpy(meta0, peers[0].bytes + 3 * sizeof(cudaIpcMemHandle_t), sizeof(meta0));
+    const int G = int(meta0[3]);
+    for (int q = 0; q < world; ++q) {
+      int64_t mq[4];
+      std::memcpy(mq, peers[q].bytes + 3 * sizeof(cudaIpcMemHandle_t), sizeof(mq));
+      if (mq[0] != in->h.n || mq[1] != in->h.np || mq[2] != in->arena_len || mq[3] != G)
+        throw hh::InputError("sharded solve: ranks hold different instances or team sizes");
+    }
+    ensure_workspace(in, G, cfg->seed, cfg->eig_block_restart);
+    std::vector<void*> opened;
+    struct Close {
+      std::vector<void*>& v;
+      ~Close() {
+        for (void* p : v) cudaIpcCloseMemHandle(p);
+      }
+    } closer{opened};
+    Params P = base_params(in, cfg);
+    P.op = kOpSolve;
+    P.s_in = upload_start(in, cfg, U0_host, s0);
+    P.p_trace = host_multiplier_to_dev(in, p0_host);
+    P.fab.world = world;
+    P.fab.me = rank;
+    P.fab.arena_len = in->arena_len;
+    P.fab.xerr = in->xerr;
+    P.I.s_col = nullptr;  // row-owner sharding keeps the CSR engines
+    P.p_sell = P.q_sell = P.r_sell = nullptr;
+    P.svc_req = nullptr;
+    for (int q = 0; q < world; ++q) {
+      if (q == rank) {
+        P.fab.xbar[q] = in->xbar;
+        P.fab.xslots[q] = in->xslots;
+        P.fab.arena[q] = in->arena;
+        continue;
+      }
+      cudaIpcMemHandle_t h[3];
+      std::memcpy(h, peers[q].bytes, sizeof(h));
+      void* ptr[3];
+      for (int t = 0; t < 3; ++t) {
+        ck(cudaIpcOpenMemHandle(&ptr[t], h[t], cudaIpcMemLazyEnablePeerAccess), "ipc open");
+        opened.push_back(ptr[t]);
+      }
+      P.fab.xbar[q] = static_cast<unsigned long long*>(ptr[0]);
+      P.fab.xslots[q] = static_cast<double*>(ptr[1]);
+      P.fab.arena[q] = static_cast<double*>(ptr[2]);
+    }
+    ck(cudaMemset(in->xerr, 0, sizeof(int)), "xerr");
+    const auto t_start = std::chrono::steady_clock::now();
+    float ms = 0.f;
+    SolveOut so{};
+    launch(in, P, G, 0, &so, &ms);
+    int xe = 0;
+    ck(cudaMemcpy(&xe, in->xerr, sizeof(int), cudaMemcpyDeviceToHost), "xerr");
+    if (xe && so.status == kOk) {
+      so.status = kErrFabric;
+      so.msg = kMsgFabric;
+    }
+    const double wall =
+        std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();
+    std::vector<cuhallar_instance*> me{in};
+    return fill_report(in, so, ms, wall, rep, sol, me);
   });
 }
 

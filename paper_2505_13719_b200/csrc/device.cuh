@@ -73,6 +73,8 @@ struct Ctx {
   int msg = kMsgNone;
   unsigned long long prof_last = 0;
   const Params* Pp = nullptr;  // launch parameters (debug hooks)
+  double deadline = 1e300;  // solve: t0 + time_limit (team_now ns), see fista_dev
+  bool timed_out = false;
   double beta = 0.0;     // current AL penalty (replicated)
   double p_trace = 0.0;  // current p[m-1] (theta trace multiplier)
 };
@@ -633,24 +635,30 @@ __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, unsigned
 // factor rows sit on the critical path (the passes are latency-bound at 16
 // warps per SM), and the streams cost no per-lane load instructions.  Same
 // fold as row_pass_sell, so results are bit-identical.
-template <int S, bool FIXED, bool HB, class UA, class Epi>
+template <int S, bool FIXED, bool HB, class UA, class Epi, bool GOP = false>
 __device__ __forceinline__ void row_pass_sell_async(Ctx& c, const Params& P, const UA& U,
                                                     const double* __restrict__ Ps, double beta,
                                                     double alpha, const double* cs, bool zero_init,
                                                     double (&sums)[3], Epi& epi) {
   static_assert(S >= 1 && S <= 4, "SELL engine: ranks 1..4");
-  constexpr int B = HB ? 4 : 8;  // per warp and stage: B x 32 x (4 + 8 [+ 8]) bytes
+  // GOP: the GradientOperator build (sdp_instance.cpp:73-83) instead of a row
+  // fold: per entry r = U_a.U_b - b, q = p + beta r written in SELL order and,
+  // for upper entries, in edge order (edge id streamed from s_eid); sums[0] =
+  // p.r, sums[1] = r.r over upper entries, sums[2] counts non-finite q
+  constexpr int B = HB ? 6 : 8;  // per warp and stage: B x 32 x (4 [+ 4] + 8 [+ 8]) bytes
   constexpr int kStageInts = B * 32;
-  static_assert((HB ? 5 : 3) * B * kThreads + 2 * kWarps <= kPassScratch,
+  constexpr int kInts = GOP ? 2 : 1;  // int32 streams (column, [edge id]) in doubles of B x 512
+  static_assert((2 * kInts + (HB ? 4 : 2)) * B * kThreads / 2 + 2 * kWarps <= kPassScratch,
                 "SELL stages exceed the pass scratch");
   const DevPairs& I = P.I;
   const int lane = c.lane, warp = c.warp;
-  // scratch: [warp][stage] col blocks (int32), p blocks, b blocks, then the barriers
+  // scratch: [warp][stage] col blocks (int32), [edge-id blocks], p blocks, b blocks, barriers
   int32_t* const colW = reinterpret_cast<int32_t*>(c.tw) + warp * 2 * kStageInts;
-  double* const pW = c.tw + B * kThreads + warp * 2 * kStageInts;
-  double* const bW = c.tw + 3 * B * kThreads + warp * 2 * kStageInts;
+  uint32_t* const eidW = reinterpret_cast<uint32_t*>(c.tw + B * kThreads) + warp * 2 * kStageInts;
+  double* const pW = c.tw + kInts * B * kThreads + warp * 2 * kStageInts;
+  double* const bW = c.tw + (kInts + 2) * B * kThreads + warp * 2 * kStageInts;
   unsigned long long* const bar =
-      reinterpret_cast<unsigned long long*>(c.tw + (HB ? 5 : 3) * B * kThreads) + warp * 2;
+      reinterpret_cast<unsigned long long*>(c.tw + (kInts + (HB ? 4 : 2)) * B * kThreads) + warp * 2;
   double csr[S];
 #pragma unroll
   for (int k = 0; k < S; ++k) csr[k] = cs ? cs[k] : 0.0;
@@ -674,8 +682,9 @@ __device__ __forceinline__ void row_pass_sell_async(Ctx& c, const Params& P, con
   auto issue = [&](int st, const Sl& x, int v0) {  // lane 0 only
     const int ne = min(B, x.L - v0) * 32;
     const int64_t g = x.s_beg + (int64_t)v0 * 32;
-    mbar_expect_tx(bar + st, (unsigned)ne * (HB ? 20u : 12u));
+    mbar_expect_tx(bar + st, (unsigned)ne * ((HB ? 20u : 12u) + (GOP ? 4u : 0u)));
     tma_load_1d(colW + st * kStageInts, I.s_col + g, ne * 4, bar + st, pol);
+    if (GOP) tma_load_1d(eidW + st * kStageInts, I.s_eid + g, ne * 4, bar + st, pol);
     tma_load_1d(pW + st * kStageInts, Ps + g, ne * 8, bar + st, pol);
     if (HB) tma_load_1d(bW + st * kStageInts, I.s_b + g, ne * 8, bar + st, pol);
   };
@@ -723,11 +732,13 @@ __device__ __forceinline__ void row_pass_sell_async(Ctx& c, const Params& P, con
         mbar_wait(bar + st, (phase >> st) & 1u);
         phase ^= 1u << st;
         int32_t bc[B];
+        uint32_t ek[B];
         double pk[B], bk[B];
 #pragma unroll
         for (int u = 0; u < B; ++u) {
           const bool ok = v0 + u < X.nv;
           bc[u] = ok ? colW[st * kStageInts + u * 32 + lane] : 0;
+          ek[u] = (ok && GOP) ? eidW[st * kStageInts + u * 32 + lane] : 0u;
           pk[u] = ok ? pW[st * kStageInts + u * 32 + lane] : 0.0;
           bk[u] = (ok && HB) ? bW[st * kStageInts + u * 32 + lane] : 0.0;
         }
@@ -747,6 +758,27 @@ __device__ __forceinline__ void row_pass_sell_async(Ctx& c, const Params& P, con
           const int v = v0 + u;
           if (v >= X.nv) break;
           const bool upper = v >= X.nlo;
+          if constexpr (GOP) {
+            double d = 0.0;
+#pragma unroll
+            for (int k = 0; k < S; ++k) {
+              const double tt = ua[k] * ub[u][k];
+              d = (k == 0) ? tt : d + tt;
+            }
+            const double rr = d - bk[u];
+            const double q = pk[u] + beta * rr;
+            const int64_t slot = X.s_beg + 32 * (int64_t)v + lane;
+            P.r_sell[slot] = rr;
+            P.q_sell[slot] = q;
+            if (!isfinite(q)) sums[2] = sums[2] + 1.0;
+            if (upper) {
+              P.r_up[ek[u]] = rr;
+              P.q_up[ek[u]] = q;
+              sums[0] = sums[0] + pk[u] * rr;
+              sums[1] = sums[1] + rr * rr;
+            }
+            continue;
+          }
           double w;
           if (FIXED) {
             w = 0.5 * pk[u];
@@ -772,7 +804,7 @@ __device__ __forceinline__ void row_pass_sell_async(Ctx& c, const Params& P, con
         }
         st ^= 1;
       }
-      if (X.mine) {
+      if (!GOP && X.mine) {
 #pragma unroll
         for (int k = 0; k < S; ++k) epi(X.a, k, acc[k], ua[k]);
       }
@@ -1172,6 +1204,33 @@ __device__ __forceinline__ void gradop_pass(Ctx& c, const Params& P, const doubl
   *nonfinite = bad;
 }
 
+// GradientOperator build on the SELL engine (single GPU, ranks 1..4, large
+// instances): q and r in SELL order (the Lanczos / FW passes read q_sell) and
+// in edge order; the lower-order copies are not written (the multiplier
+// update re-gathers p_lo from p_up, bit-identical).  Returns false when the
+// SELL path does not apply (the caller runs gradop_pass).
+template <int S>
+__device__ __forceinline__ bool gradop_sell(Ctx& c, const Params& P, const double* __restrict__ U,
+                                            double beta, double (&sums)[2], bool* nonfinite) {
+  if constexpr (S >= 1 && S <= 4) {
+    const DevPairs& I = P.I;
+    if (!I.s_col || !P.q_sell || !P.r_sell || c.rh - c.rl < kRtMinRows || !sell_aligned<S>(U)) return false;
+    double s3[3] = {0.0, 0.0, 0.0};
+    auto none = [](int64_t, int, double, double) {};
+    if (I.s_b)
+      row_pass_sell_async<S, false, true, UPlain, decltype(none), true>(c, P, UPlain{U}, P.p_sell, beta, 0.0,
+                                                                         nullptr, true, s3, none);
+    else
+      row_pass_sell_async<S, false, false, UPlain, decltype(none), true>(c, P, UPlain{U}, P.p_sell, beta, 0.0,
+                                                                          nullptr, true, s3, none);
+    sums[0] = s3[0];
+    sums[1] = s3[1];
+    *nonfinite = s3[2] != 0.0;
+    return true;
+  }
+  return false;
+}
+
 // ------------------------------------------------------------- map pass ---
 // Thread per pair constraint k (edge order): d_k = U_{i_k}.U_{j_k} summed over
 // columns in order (instances.cpp:27-35).  kUnroll constraints per thread are
@@ -1420,6 +1479,8 @@ __device__ __noinline__ bool al_value_dev(Ctx& c, const Params& P, const double*
   return true;
 }
 
+inline __device__ __noinline__ double team_now(Ctx& c);  // solver.cuh
+
 // ------------------------------------------------------------ ADAP-FISTA ---
 struct Roles {
   int rep, yt, wp, best, x, y, xt, gt, yn, v, tmp;
@@ -1476,6 +1537,17 @@ __device__ __noinline__ bool fista_dev(Ctx& c, const Params& P, Roles& R, int s,
     if (c.t.xfailed) {
       fail(c, kErrFabric, kMsgFabric);
       return false;
+    }
+    // time_limit inside long FISTA runs: the reference checks it per outer
+    // iteration and per FW step (solver.cpp:141, hlr.cpp:106), which a single
+    // HLR call of a large instance can overshoot by minutes; every 512
+    // iterations the team reads CTA 0's clock and stops like an iteration limit
+    if ((it & 511) == 511 && c.deadline < 1e300 && team_now(c) >= c.deadline) {
+      c.timed_out = true;
+      out.status = 2;
+      out.L = L;
+      out.iters = it;
+      return true;
     }
     const int cap = cf.fista_max_iters > 0
                         ? cf.fista_max_iters
@@ -1783,6 +1855,11 @@ __device__ __noinline__ bool aipp_dev(Ctx& c, const Params& P, Roles& R, int s, 
       FistaOut fo;
       if (!fista_dev<S>(c, P, R, s, lambda, fmax(1.0, M_bar / 2.0), fo)) return false;
       out.fista_iters += fo.iters;
+      if (c.timed_out) {  // time_limit reached inside FISTA: unwind like an iteration limit
+        out.status = 2;
+        if (have_best) out.w_buf = R.best;
+        return true;
+      }
       if (P.cfg.trace >= 2 && P.trace && c.t.rank == 0 && threadIdx.x == 0) {
         // debug (cfg.trace >= 2): one event per fista() call, kind 9 (L0 in
         // eps_inner, status in rank, iterations in outer_iter, final L in gap,

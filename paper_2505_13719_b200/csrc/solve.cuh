@@ -103,6 +103,7 @@ inline __device__ __noinline__ void solve_dev(Ctx& c, const Params& P, SolveOut*
   const Cfg& cf = P.cfg;
   const double t0 = team_now(c);
   const double deadline = t0 + cf.time_limit * 1e9;
+  c.deadline = deadline;
   if (c.t.rank == 0 && threadIdx.x == 0) c.prof_last = gtimer_ns();
   const double nb1 = I.norm_b1, nb2 = I.nb2;
   const double eps_floor = cf.eps_floor > 0 ? cf.eps_floor : cf.eps * (1.0 + nb1) / 10.0;
@@ -180,8 +181,9 @@ inline __device__ __noinline__ void solve_dev(Ctx& c, const Params& P, SolveOut*
       if (!is_pr(I)) {
         const int64_t lo_n = I.lo_ptr[c.rh] - I.lo_ptr[c.rl];
         const int64_t lo0 = I.lo_ptr[c.rl];
-        for (int64_t e = threadIdx.x; e < lo_n; e += kThreads)
-          P.p_lo[lo0 + e] = P.p_lo[lo0 + e] + beta * P.r_lo[lo0 + e];
+        if (!P.p_sell)  // (SELL mode: r_lo is not built; p_lo is re-gathered below)
+          for (int64_t e = threadIdx.x; e < lo_n; e += kThreads)
+            P.p_lo[lo0 + e] = P.p_lo[lo0 + e] + beta * P.r_lo[lo0 + e];
         if (P.p_sell) {  // the SELL copy, warp per slice (coalesced)
           for (int64_t sl = (c.rl >> 5) + c.warp; sl < ((c.rh + 31) >> 5); sl += kWarps) {
             const int64_t a = (sl << 5) + c.lane;
@@ -204,6 +206,14 @@ inline __device__ __noinline__ void solve_dev(Ctx& c, const Params& P, SolveOut*
       team_sum<2>(c.t, c.rs, v);
       bp = v[0];
       bad = v[1];
+      if (P.p_sell && !is_pr(I)) {
+        // p_lo = p_up in lower order: exactly p_lo + beta r_lo (the lower copy
+        // of r_k rounds like the upper one); p_up is complete after the sum above
+        const int64_t lo_n = I.lo_ptr[c.rh] - I.lo_ptr[c.rl];
+        const int64_t lo0 = I.lo_ptr[c.rl];
+        for (int64_t e = threadIdx.x; e < lo_n; e += kThreads) P.p_lo[lo0 + e] = P.p_up[I.lo_eid[lo0 + e]];
+        __syncthreads();
+      }
     }
     c.p_trace = c.p_trace + beta * ho.rt;
     theta = ho.theta;

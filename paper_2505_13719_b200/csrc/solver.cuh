@@ -261,7 +261,20 @@ __device__ __forceinline__ void lz_dot_rows(Ctx& c, const Params& P, int k, doub
     double acc[8];
 #pragma unroll
     for (int u = 0; u < 8; ++u) acc[u] = 0.0;
-    for (int64_t a = c.rl + threadIdx.x; a < c.rh; a += kThreads) {
+    // two rows per step: 16 independent loads in flight per thread
+    int64_t a = c.rl + threadIdx.x;
+    for (; a + kThreads < c.rh; a += 2 * kThreads) {
+      const double wa = w[a], wb = w[a + kThreads];
+      double va[8], vb[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        va[u] = g + u < k ? v[u][a] : 0.0;
+        vb[u] = g + u < k ? v[u][a + kThreads] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) acc[u] = (acc[u] + va[u] * wa) + vb[u] * wb;
+    }
+    if (a < c.rh) {
       const double wa = w[a];
 #pragma unroll
       for (int u = 0; u < 8; ++u)
@@ -683,7 +696,7 @@ __device__ __noinline__ bool gradop_dev(Ctx& c, const Params& P, const double* Y
       sums[1] = sums[1] + r * r;
     });
   } else {
-    gradop_pass<S>(c, P, Y, s, beta, sums, &bad);
+    if (!gradop_sell<S>(c, P, Y, beta, sums, &bad)) gradop_pass<S>(c, P, Y, s, beta, sums, &bad);
   }
   double v[3] = {sums[0], sums[1], bad ? 1.0 : 0.0};
   team_sum<3>(c.t, c.rs, v);

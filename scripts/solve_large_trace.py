@@ -33,8 +33,22 @@ def main():
     inst = build(a.name)
     gen = time.perf_counter() - t0
     ev = []
+    t_solve = time.perf_counter()
+    fcalls = [0, 0]
+
+    def sink(e):  # live: progress survives a killed run
+        ev.append(e)
+        if e.kind == "fista_debug":
+            fcalls[0] += 1
+            fcalls[1] += e.outer_iter
+        elif e.kind == "outer":
+            print(json.dumps({"t": round(time.perf_counter() - t_solve, 1), "outer": e.outer_iter,
+                              "beta": e.beta, "rank": e.rank, "rel_pfeas": e.rel_pfeas,
+                              "rel_gap": e.rel_gap, "fista_calls": fcalls[0], "fista_iters": fcalls[1]}),
+                  file=sys.stderr, flush=True)
+
     cfg = H.SolverConfig(eps=1e-5, seed=0, time_limit=a.time_limit, profile=True, parity=a.parity)
-    r = H.solve(inst, cfg, sink=ev.append, fetch=False)
+    r = H.solve(inst, cfg, sink=sink, fetch=False)
     outer, cur = [], {"calls": 0, "iters": 0, "success": 0, "failure": 0, "limit": 0, "L_max": 0.0,
                       "lambda_min": None}
     for e in ev:

@@ -82,3 +82,20 @@ def test_sharded_rejects_phase_retrieval(H):
     insts = [H.gen_phase_retrieval(H.PrSpec(8, 4, seed=1)) for _ in range(2)]
     with pytest.raises(H.InputError):
         H.solve_sharded(insts)
+
+
+def test_solve_rank_world1_matches_plain_solve(H):
+    """The one-process-per-GPU entry points (cuhallar_shard_export /
+    cuhallar_solve_rank, used by bench.py under torchrun) at world 1: the IPC
+    handle round trip and the rank launch reproduce the plain solve."""
+    inst = H.build_theta_instance(H.make_hypercube(6))
+    cfg = H.SolverConfig(eps=1e-5, seed=0)
+    ref = H.solve(inst, cfg)
+    hb = H.shard_export(inst)
+    assert isinstance(hb, bytes) and len(hb) == 512
+    r = H.solve_rank(inst, 1, 0, [hb], cfg, fetch=True)
+    assert r.status == ref.status == "optimal"
+    assert abs(r.pval - ref.pval) <= 1e-6 * max(1.0, abs(ref.pval))
+    assert r.rank == ref.rank
+    with pytest.raises(H.InputError):
+        H.solve_rank(inst, 2, 0, [hb], cfg)  # a peer blob is missing

@@ -167,6 +167,7 @@ struct cuhallar_instance {
   double* svc_buf_h = nullptr;
   hd::DevSell sell;  // SELL-32 row-stream copy (single-GPU row passes), optional
   double *s_b = nullptr, *s_ub = nullptr, *p_sell = nullptr, *q_sell = nullptr, *r_sell = nullptr;
+  double* pad = nullptr;  // n x 4 padded rank-3 factor rows (SELL passes)
   int n_refill = 0;
   uint64_t lz_seed = ~0ull;
   double* dscal = nullptr;
@@ -187,7 +188,7 @@ struct cuhallar_instance {
     f(masks); f(twid); f(prF); f(prG); f(gA);
     f(bar); f(slots); f(arena); f(xbar); f(xslots); f(xerr);
     f(p_up); f(p_lo); f(q_up); f(q_lo); f(r_up); f(r_lo); f(lz_rand); f(dscal); f(discal); f(dso); f(dprof);
-    f(sell.off); f(sell.nlo); f(sell.nv); f(sell.col); f(sell.eid); f(s_b); f(s_ub); f(p_sell); f(q_sell); f(r_sell);
+    f(sell.off); f(sell.nlo); f(sell.nv); f(sell.col); f(sell.eid); f(s_b); f(s_ub); f(pad); f(p_sell); f(q_sell); f(r_sell);
     if (trace_host) cudaFreeHost(trace_host);
     if (svc_req_h) cudaFreeHost(svc_req_h);
     if (svc_ready_h) cudaFreeHost(svc_ready_h);
@@ -233,6 +234,7 @@ void build_sell(cuhallar_instance* in) {
   hd::sell_fill_device(h.n, in->up_ptr, in->lo_ptr, in->ej, in->lo_col, in->lo_eid, &sl, 0);
   in->sell = sl;
   in->bytes += slots * 8 + (sl.nslices + 1) * 8 + h.n * 8;
+  in->pad = dalloc<double>(size_t(h.n) * 4, &in->bytes);
   in->p_sell = dalloc<double>(size_t(slots), &in->bytes);
   in->q_sell = dalloc<double>(size_t(slots), &in->bytes);
   in->r_sell = dalloc<double>(size_t(slots), &in->bytes);
@@ -617,7 +619,7 @@ const char* msg_text(int id) {
 Params base_params(cuhallar_instance* in, const cuhallar_config* cfg) {
   Params P;
   P.I = in->I;
-  P.pass_scratch = in->gA ? 8 * kGprChunk  // staged DMMA right-hand side
+  P.pass_scratch = in->gA ? kGprLd * kGprChunk  // staged DMMA right-hand side
                   : in->h.family == kPhaseret
                       ? int(std::max<int64_t>(2 * in->h.nc, 1024))
                       : (in->sell.col ? kPassScratch  // SELL stages (row_pass_sell_async)
@@ -653,6 +655,7 @@ Params base_params(cuhallar_instance* in, const cuhallar_config* cfg) {
   P.p_sell = in->p_sell;
   P.q_sell = in->q_sell;
   P.r_sell = in->r_sell;
+  P.pad = in->pad;
   P.scalars = in->dscal;
   P.iscalars = in->discal;
   P.trace = nullptr;
@@ -752,6 +755,7 @@ int launch(cuhallar_instance* in, Params& P, int grid, cudaStream_t st, SolveOut
   if (par || P.fab.world > 1) {  // the SELL engine serves single-GPU fast-mode passes only
     P.I.s_col = nullptr;
     P.p_sell = P.q_sell = P.r_sell = nullptr;
+    P.pad = nullptr;
   }
   std::unique_ptr<RefillService> svc;
   if (P.svc_req && P.fab.world == 1 && (P.op == kOpSolve || P.op == kOpMinEigG || P.op == kOpAipp))
@@ -762,8 +766,7 @@ int launch(cuhallar_instance* in, Params& P, int grid, cudaStream_t st, SolveOut
                                  dim3(grid), dim3(kThreads), args, smem_bytes(P.pass_scratch), st),
      "cooperative launch");
   if (ms) ck(cudaEventRecord(e1, st), "event");
-  ck(cudaMemcpyAsync(so, in->dso, sizeof(SolveOut), cudaMemcpyDeviceToHost, st), "D2H out");
-  if (poll) {  // e.g. trace events delivered while the solve runs
+  if (poll) {  // e.g. trace events delivered while the solve runs (before any blocking copy)
     cudaError_t q;
     while ((q = cudaStreamQuery(st)) == cudaErrorNotReady) {
       poll();
@@ -771,6 +774,7 @@ int launch(cuhallar_instance* in, Params& P, int grid, cudaStream_t st, SolveOut
     }
     if (q != cudaSuccess) ck(q, "hallar_kernel");
   }
+  ck(cudaMemcpyAsync(so, in->dso, sizeof(SolveOut), cudaMemcpyDeviceToHost, st), "D2H out");
   ck(cudaStreamSynchronize(st), "hallar_kernel");
   svc.reset();
   if (ms) {

@@ -180,6 +180,7 @@ struct Params {
   double* q_lo = nullptr;
   double* r_up = nullptr;
   double* r_lo = nullptr;
+  double* pad = nullptr;     // n x 4: rank-3 factor rows padded to 32 B for 256-bit gathers (SELL)
   double* p_sell = nullptr;  // the same multipliers in SELL slot order (null: no SELL copy)
   double* q_sell = nullptr;
   double* r_sell = nullptr;

@@ -464,10 +464,38 @@ __device__ __forceinline__ void row_pass_rt(Ctx& c, const Params& P, const UA& U
 // s = 4: 256-bit, s = 3: 64 + 128-bit), so a gathered row costs one L1
 // wavefront per entry; the streams are read evict-first (__ldcs) so the
 // gathered factor stays L2-resident.
+// A rank-3 factor copied to rows of 4 doubles (P.pad): one 256-bit load per
+// gathered row instead of a 64-bit + a 128-bit one (the gathers are
+// L1-wavefront bound).  Filled by pad_rows before a pass, read-only in it.
+struct UPad4 {
+  const double* __restrict__ U;
+  __device__ __forceinline__ double operator()(int64_t o) const { return U[(o / 3) * 4 + o % 3]; }
+  __device__ __forceinline__ const double* base() const { return U; }
+  __device__ __forceinline__ double xf(double raw) const { return raw; }
+};
+template <class UA>
+struct URowStride {
+  static constexpr int v = 0;  // the rank
+};
+template <>
+struct URowStride<UPad4> {
+  static constexpr int v = 4;
+};
+
 template <int S, class UA>
 __device__ __forceinline__ void sell_row(const UA& U, int64_t b, double (&o)[S]) {
-  const double* p = U.base() + b * S;
-  if constexpr (S == 1) {
+  constexpr int ST = URowStride<UA>::v ? URowStride<UA>::v : S;
+  const double* p = U.base() + b * ST;
+  if constexpr (ST == 4 && S == 3) {
+    double t0, t1, t2, t3;
+    asm volatile("ld.global.v4.f64 {%0,%1,%2,%3}, [%4];"
+                 : "=d"(t0), "=d"(t1), "=d"(t2), "=d"(t3)
+                 : "l"(p));
+    (void)t3;
+    o[0] = t0;
+    o[1] = t1;
+    o[2] = t2;
+  } else if constexpr (S == 1) {
     o[0] = U.xf(p[0]);
   } else if constexpr (S == 2) {
     const double2 v = *reinterpret_cast<const double2*>(p);
@@ -500,6 +528,19 @@ template <int S>
 __device__ __forceinline__ bool sell_aligned(const double* base) {
   const unsigned long long a = reinterpret_cast<unsigned long long>(base);
   return S == 1 || (S == 4 ? (a & 31) == 0 : (a & 15) == 0);
+}
+
+// rows [rl, rh) of a rank-3 factor -> P.pad (stride 4), then a team barrier
+// (the pass that follows gathers every row)
+template <class UA>
+__device__ __forceinline__ void pad_rows3(Ctx& c, const Params& P, const UA& U) {
+  for (int64_t a = c.rl + threadIdx.x; a < c.rh; a += kThreads) {
+    const double u0 = U(a * 3), u1 = U(a * 3 + 1), u2 = U(a * 3 + 2);
+    double* d = P.pad + a * 4;
+    *reinterpret_cast<double2*>(d) = make_double2(u0, u1);
+    d[2] = u2;
+  }
+  c.t.sync();
 }
 
 template <int S, bool FIXED, class UA, class Epi>
@@ -853,8 +894,26 @@ __device__ __forceinline__ void row_pass_t(Ctx& c, const Params& P, const UA& U,
   publish_rows(c.t, U.base(), c.rl, c.rh, s);  // sharded: gathered rows -> every rank
   if constexpr (S >= 1 && S <= 4) {
     // many rows per CTA: the row-thread engine (same arithmetic, bit-exact)
+    const double* Ps = sell_of(P, Pup);
+    if constexpr (S == 3) {
+      // (team-uniform condition: pad_rows3 synchronises the team)
+      {
+        if (Ps && P.pad) {  // 256-bit gathers from the padded copy
+          pad_rows3(c, P, U);
+          const UPad4 Up{P.pad};
+          if constexpr (!FIXED) {
+            if (I.s_b)
+              row_pass_sell_async<S, false, true>(c, P, Up, Ps, beta, alpha, cs, zero_init, sums, epi);
+            else
+              row_pass_sell_async<S, false, false>(c, P, Up, Ps, beta, alpha, cs, zero_init, sums, epi);
+          } else {
+            row_pass_sell_async<S, true, false>(c, P, Up, Ps, beta, alpha, cs, zero_init, sums, epi);
+          }
+          return;
+        }
+      }
+    }
     if (c.rh - c.rl >= kRtMinRows) {
-      const double* Ps = sell_of(P, Pup);
       if (Ps && sell_aligned<S>(U.base())) {
         if constexpr (!FIXED) {
           if (I.s_b)
@@ -1214,15 +1273,33 @@ __device__ __forceinline__ bool gradop_sell(Ctx& c, const Params& P, const doubl
                                             double beta, double (&sums)[2], bool* nonfinite) {
   if constexpr (S >= 1 && S <= 4) {
     const DevPairs& I = P.I;
-    if (!I.s_col || !P.q_sell || !P.r_sell || c.rh - c.rl < kRtMinRows || !sell_aligned<S>(U)) return false;
+    // team-uniform conditions only (pad_rows3 synchronises the team); the
+    // SELL engine is correct for any row range
+    if (!I.s_col || !P.q_sell || !P.r_sell || !sell_aligned<S>(U)) return false;
     double s3[3] = {0.0, 0.0, 0.0};
     auto none = [](int64_t, int, double, double) {};
-    if (I.s_b)
-      row_pass_sell_async<S, false, true, UPlain, decltype(none), true>(c, P, UPlain{U}, P.p_sell, beta, 0.0,
-                                                                         nullptr, true, s3, none);
-    else
-      row_pass_sell_async<S, false, false, UPlain, decltype(none), true>(c, P, UPlain{U}, P.p_sell, beta, 0.0,
-                                                                          nullptr, true, s3, none);
+    bool done = false;
+    if constexpr (S == 3) {
+      if (P.pad) {
+        pad_rows3(c, P, UPlain{U});
+        const UPad4 Up{P.pad};
+        if (I.s_b)
+          row_pass_sell_async<S, false, true, UPad4, decltype(none), true>(c, P, Up, P.p_sell, beta, 0.0,
+                                                                            nullptr, true, s3, none);
+        else
+          row_pass_sell_async<S, false, false, UPad4, decltype(none), true>(c, P, Up, P.p_sell, beta, 0.0,
+                                                                             nullptr, true, s3, none);
+        done = true;
+      }
+    }
+    if (!done) {
+      if (I.s_b)
+        row_pass_sell_async<S, false, true, UPlain, decltype(none), true>(c, P, UPlain{U}, P.p_sell, beta, 0.0,
+                                                                           nullptr, true, s3, none);
+      else
+        row_pass_sell_async<S, false, false, UPlain, decltype(none), true>(c, P, UPlain{U}, P.p_sell, beta,
+                                                                            0.0, nullptr, true, s3, none);
+    }
     sums[0] = s3[0];
     sums[1] = s3[1];
     *nonfinite = s3[2] != 0.0;
@@ -1276,6 +1353,16 @@ __device__ __forceinline__ void map_pass_src(Ctx& c, const Params& P, const RowS
   const DevPairs& I = P.I;
   const int s = S > 0 ? S : s_rt;
   if (src.U) publish_rows(c.t, src.U, c.rl, c.rh, s);
+  if constexpr (S == 3) {
+    if (I.s_col && P.pad) {  // large single-GPU instance: 256-bit gathers from the padded copy
+      if (src.U) {
+        pad_rows3(c, P, UPlain{src.U});
+      } else {
+        pad_rows3(c, P, [&](int64_t o) { return src.at(o); });
+      }
+    }
+  }
+  const bool padded = S == 3 && I.s_col && P.pad;
   for (int64_t k0 = c.kl + threadIdx.x; k0 < c.kh; k0 += (int64_t)kThreads * kUnroll) {
     int64_t ii[kUnroll], jj[kUnroll];
     double pk[kUnroll], bk[kUnroll], rf[kUnroll];
@@ -1296,8 +1383,13 @@ __device__ __forceinline__ void map_pass_src(Ctx& c, const Params& P, const RowS
       if constexpr (S > 0 && S <= 4) {
         // both rows with the widest aligned vector loads (sell_row)
         double ri[S], rj[S];
-        src.row<S>(ii[u], ri);
-        src.row<S>(jj[u], rj);
+        if (padded) {
+          sell_row<S>(UPad4{P.pad}, ii[u], ri);
+          sell_row<S>(UPad4{P.pad}, jj[u], rj);
+        } else {
+          src.row<S>(ii[u], ri);
+          src.row<S>(jj[u], rj);
+        }
 #pragma unroll
         for (int cc = 0; cc < S; ++cc) {
           const double t = ri[cc] * rj[cc];

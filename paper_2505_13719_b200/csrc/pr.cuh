@@ -108,8 +108,19 @@ __device__ __forceinline__ void dmma884(double (&d)[2], double a, double b) {
                : "+d"(d[0]), "+d"(d[1])
                : "d"(a), "d"(b));
 }
-constexpr int kGprChunk = 512;  // rows of the staged right-hand side (x 8 doubles)
+constexpr int kGprChunk = 512;  // rows of the staged right-hand side
+constexpr int kGprLd = 10;      // its row stride in doubles (8 used): conflict-free fragment reads
 
+__device__ __forceinline__ void ldg4_f64(const double* p, double (&o)[4]) {
+  asm volatile("ld.global.cs.v4.f64 {%0,%1,%2,%3}, [%4];"
+               : "=d"(o[0]), "=d"(o[1]), "=d"(o[2]), "=d"(o[3])
+               : "l"(p));
+}
+
+// Forward: each lane streams 4 consecutive k of its row of A' with one
+// 256-bit load and feeds them to 4 DMMA steps (the k order inside a step is
+// permuted accordingly: lane quad q supplies k = 4q + t in step t, and reads
+// the matching right-hand-side rows), 4 such loads in flight per lane.
 template <class UA>
 __device__ __noinline__ void gpr_forward(const Params& P, int rank, int size, double* Ws, const UA U,
                                          int s) {
@@ -117,13 +128,15 @@ __device__ __noinline__ void gpr_forward(const Params& P, int rank, int size, do
   const int64_t n = I.nc, n2 = 2 * I.nc, m = I.m;
   const double* __restrict__ A = I.gA;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int kq = lane & 3, cq = lane >> 2;
+  const bool vec = (n & 1) == 0;  // rows of A' 32-byte aligned
   const int ng = (s + 3) / 4;
   const int64_t nblk = (m + 8 * kWarps - 1) / (8 * kWarps);
   for (int64_t item = rank; item < nblk * ng; item += size) {
     const int64_t blk = item / ng;
     const int c0 = (int)(item % ng) * 4, sc = min(4, s - c0);
-    const int64_t row = blk * 8 * kWarps + warp * 8 + (lane >> 2);
-    const double* ar = A + (row < m ? row : m - 1) * n2 + (lane & 3);
+    const int64_t row = blk * 8 * kWarps + warp * 8 + cq;
+    const double* ar = A + (row < m ? row : m - 1) * n2;
     double acc[2] = {0.0, 0.0}, acc2[2] = {0.0, 0.0};
     for (int64_t k0 = 0; k0 < n2; k0 += kGprChunk) {
       __syncthreads();
@@ -138,18 +151,28 @@ __device__ __noinline__ void gpr_forward(const Params& P, int rank, int size, do
           else
             v = k < n ? U((n + k) * s + col) : -U((k - n) * s + col);
         }
-        Ws[idx] = v;
+        Ws[kk * kGprLd + cc] = v;
       }
       __syncthreads();
       const int kmax = (int)min((int64_t)kGprChunk, n2 - k0);
 #pragma unroll 4
-      for (int kk = 0; kk < kmax; kk += 8) {
-        const bool ok0 = row < m && k0 + kk + (lane & 3) < n2;
-        const bool ok1 = row < m && k0 + kk + 4 + (lane & 3) < n2;
-        const double a0 = ok0 ? __ldcs(ar + k0 + kk) : 0.0;
-        const double a1 = ok1 ? __ldcs(ar + k0 + kk + 4) : 0.0;
-        dmma884(acc, a0, Ws[(kk + (lane & 3)) * 8 + (lane >> 2)]);
-        dmma884(acc2, a1, Ws[(kk + 4 + (lane & 3)) * 8 + (lane >> 2)]);
+      for (int kk = 0; kk < kmax; kk += 16) {
+        const int64_t kb = k0 + kk + 4 * kq;
+        double a[4];
+        if (vec && row < m && kb + 3 < n2) {
+          ldg4_f64(ar + kb, a);
+        } else {
+#pragma unroll
+          for (int t = 0; t < 4; ++t) a[t] = (row < m && kb + t < n2) ? ar[kb + t] : 0.0;
+        }
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          const double b = Ws[(kk + 4 * kq + t) * kGprLd + cq];
+          if (t & 1)
+            dmma884(acc2, a[t], b);
+          else
+            dmma884(acc, a[t], b);
+        }
       }
     }
     // lane holds Y[row][2 tq + e], tq = lane & 3: tq 0/1 real parts of columns
@@ -216,18 +239,18 @@ __device__ __noinline__ void gpr_inverse(const Params& P, int rank, int size, do
           const double2 f = I.F[(int64_t)(c0 + cl) * m + i];
           v = cc < 4 ? f.x * q : f.y * q;
         }
-        Ws[idx] = v;
+        Ws[ii * kGprLd + cc] = v;
       }
       __syncthreads();
       if (j0 < n) {
         const int imax = (int)min((int64_t)kGprChunk, i_hi - ib);
-#pragma unroll 4
+#pragma unroll 8
         for (int ii = 0; ii < imax; ii += 4) {
           const int64_t i = ib + ii + (lane & 3);
           const bool ok = jok && i < i_hi;
           const double a1 = ok ? __ldcs(A + i * n2 + jr) : 0.0;
           const double a2 = ok ? __ldcs(A + i * n2 + n + jr) : 0.0;
-          const double b = Ws[(ii + (lane & 3)) * 8 + (lane >> 2)];
+          const double b = Ws[(ii + (lane & 3)) * kGprLd + (lane >> 2)];
           dmma884(d1, a1, b);
           dmma884(d2, a2, b);
         }

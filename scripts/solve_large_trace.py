@@ -20,6 +20,9 @@ def build(name):
     if name.startswith("mc"):
         n1, n2, r = [int(x) for x in name[2:].split("_")]
         return H.gen_matrix_completion(H.McSpec(n1, n2, r, seed=0))
+    if name.startswith("pr"):
+        nc, L = [int(x) for x in name[2:].split("_")]
+        return H.gen_phase_retrieval(H.PrSpec(nc, L, seed=0))
     raise KeyError(name)
 
 

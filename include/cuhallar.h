@@ -31,7 +31,10 @@ enum {
   CUHALLAR_ERR_INPUT = 64,
   CUHALLAR_ERR_NUMERICAL = 3,
   CUHALLAR_ERR_IO = 66,
-  CUHALLAR_ERR_CUDA = 70
+  CUHALLAR_ERR_CUDA = 70,
+  /* a device capacity was exceeded (factor rank above 32, Lanczos slots, an
+   * unanswered refill request): not a CUDA fault; the message names the cap */
+  CUHALLAR_ERR_CAPACITY = 71
 };
 
 /* SdpInstance::field_kind (sdp_instance.hpp:11) */

@@ -51,6 +51,11 @@ class NumericalError(RuntimeError):
     """lrsdp::NumericalError (types.hpp:20-23)."""
 
 
+class CapacityError(RuntimeError):
+    """A device capacity was exceeded (status 71: factor rank above 32, Lanczos
+    slots); not a CUDA fault."""
+
+
 class CudaError(RuntimeError):
     pass
 
@@ -65,6 +70,8 @@ def _check(rc: int):
         raise NumericalError(msg)
     if rc == 66:
         raise OSError(msg)
+    if rc == 71:
+        raise CapacityError(msg)
     raise CudaError(f"cuhallar error {rc}: {msg}")
 
 

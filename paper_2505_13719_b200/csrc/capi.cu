@@ -790,6 +790,7 @@ int status_to_rc(int st, int msg) {
   g_err = msg_text(msg);
   if (st == kErrNumerical) return CUHALLAR_ERR_NUMERICAL;
   if (st == kErrInput) return CUHALLAR_ERR_INPUT;
+  if (st == kErrCapacity) return CUHALLAR_ERR_CAPACITY;
   return CUHALLAR_ERR_CUDA;
 }
 

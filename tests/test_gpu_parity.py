@@ -172,13 +172,22 @@ def test_solve_deterministic_and_warm(H, orc):
 
 
 def test_trace_events(H, orc):
+    """Fast-mode trace (trace.hpp:12-26) against the oracle's on C5, whose
+    counters agree: same event kinds, outer iterations, ranks and penalties,
+    values to 1e-9."""
     inst = H.build_theta_instance(H.make_cycle(5))
     ev = []
     rep = H.solve(inst, sink=ev.append)
     outer = [e for e in ev if e.kind == "outer"]
     assert len(outer) == rep.outer_iters and all(e.theta >= 0 for e in outer)
-    ref = []
-    orc.OracleInstance.cycle(5).solve(trace=True)
+    kinds = {0: "inner_stationary", 1: "inner_rank_step", 2: "outer"}
+    o = orc.OracleInstance.cycle(5).solve(trace=True)
+    dev = [e for e in ev if e.kind in kinds.values()]
+    assert [(e.kind, e.outer_iter, e.rank, e.beta) for e in dev] == \
+        [(kinds[e["kind"]], e["outer_iter"], e["rank"], e["beta"]) for e in o.trace]
+    for e, f in zip(dev, o.trace):
+        assert abs(e.al_value - f["al_value"]) <= 1e-9 * max(1.0, abs(f["al_value"]))
+        assert abs(e.rel_pfeas - f["rel_pfeas"]) <= 1e-9
 
 
 def test_matcomp_paper_rule_instance_and_solve(H, orc):

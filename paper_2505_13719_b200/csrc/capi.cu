@@ -252,6 +252,21 @@ void build_sell(cuhallar_instance* in) {
   I.s_b = in->s_b;
   I.s_eid = sl.eid;
   I.s_slots = slots;
+  // matrix completion: rows <= max i_k = ei[np-1] (edges sorted by (i, j)) hold
+  // every upper entry -> the row-ordered map pass (device.cuh map_pass_sell);
+  // CUHALLAR_NO_SELL_MAP=1 keeps the edge-order map (A/B runs)
+  // cost-balanced CTA row split (kernel_setup.cuh); CUHALLAR_EVEN_TILES=1
+  // keeps equal tile counts (A/B runs).  64 entries per row: a row's share of
+  // the row-wise passes (CGS2, BLAS-1, epilogues) measured against an entry's
+  // share of the row passes at C4 (profiles/r02/profile_c4_phases_final.jsonl)
+  const char* et = std::getenv("CUHALLAR_EVEN_TILES");
+  if (!(et && *et && *et != '0')) I.split_w = 64;
+  const char* em = std::getenv("CUHALLAR_NO_SELL_MAP");
+  if (h.family == kMatcomp && !h.has_trace && h.np > 0 && in->s_b && !(em && *em && *em != '0')) {
+    int32_t last = 0;
+    ck(cudaMemcpy(&last, in->ei + (h.np - 1), sizeof(int32_t), cudaMemcpyDeviceToHost), "ei tail");
+    I.s_up_slices = (int64_t(last) + 32) / 32;
+  }
 }
 
 // Device structure of a pair instance (devgen.cu builds it on the GPU):
@@ -756,6 +771,7 @@ int launch(cuhallar_instance* in, Params& P, int grid, cudaStream_t st, SolveOut
     P.I.s_col = nullptr;
     P.p_sell = P.q_sell = P.r_sell = nullptr;
     P.pad = nullptr;
+    P.I.split_w = -1;  // the parity / sharded kernels keep equal tile counts
   }
   std::unique_ptr<RefillService> svc;
   if (P.svc_req && P.fab.world == 1 && (P.op == kOpSolve || P.op == kOpMinEigG || P.op == kOpAipp))
@@ -1478,6 +1494,7 @@ int cuhallar_solve_sharded(cuhallar_instance* const* insts, int world, const cuh
       P.fab.world = world;
       P.fab.me = r;
       P.I.s_col = nullptr;  // row-owner sharding keeps the CSR engines
+      P.I.split_w = -1;
       P.p_sell = P.q_sell = P.r_sell = nullptr;
       P.svc_req = nullptr;  // refills: the pre-drawn ones only
       P.fab.arena_len = in->arena_len;
@@ -1602,6 +1619,7 @@ int cuhallar_solve_rank(cuhallar_instance* in, int world, int rank, const cuhall
     P.fab.arena_len = in->arena_len;
     P.fab.xerr = in->xerr;
     P.I.s_col = nullptr;  // row-owner sharding keeps the CSR engines
+      P.I.split_w = -1;
     P.p_sell = P.q_sell = P.r_sell = nullptr;
     P.svc_req = nullptr;
     for (int q = 0; q < world; ++q) {

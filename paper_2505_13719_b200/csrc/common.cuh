@@ -98,6 +98,12 @@ struct DevPairs {
   const double* s_b = nullptr;      // slot -> scaled b (matrix completion)
   const uint32_t* s_eid = nullptr;  // slot -> edge id (padding 0xffffffff)
   int64_t s_slots = 0;
+  // matrix completion: slices [0, s_up_slices) hold every upper entry (rows
+  // i_k < n1), later slices none (the row-ordered map pass); 0 = not used
+  int64_t s_up_slices = 0;
+  // CTA row split (one GPU, SELL instances): < 0 = equal tile counts; >= 0 =
+  // equal cost, cost(rows [0, r)) = entries + split_w * r (kernel_setup.cuh)
+  int split_w = -1;
   // phase retrieval (family kPhaseret): np = m, b_up = b (constraint order)
   int64_t nc = 0;                 // complex dimension (n = 2 nc)
   int L = 0, lognc = 0;           // masks, log2(nc)

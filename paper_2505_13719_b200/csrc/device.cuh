@@ -686,10 +686,13 @@ __device__ __forceinline__ void row_pass_sell_async(Ctx& c, const Params& P, con
   // fold: per entry r = U_a.U_b - b, q = p + beta r written in SELL order and,
   // for upper entries, in edge order (edge id streamed from s_eid); sums[0] =
   // p.r, sums[1] = r.r over upper entries, sums[2] counts non-finite q
-  constexpr int B = HB ? 6 : 8;  // per warp and stage: B x 32 x (4 [+ 4] + 8 [+ 8]) bytes
+  // per warp and stage: B x 32 x (4 [+ 4] + 8 [+ 8]) bytes; two stages per warp
+  constexpr int B = GOP ? (HB ? 5 : 7) : (HB ? 6 : 8);
   constexpr int kStageInts = B * 32;
   constexpr int kInts = GOP ? 2 : 1;  // int32 streams (column, [edge id]) in doubles of B x 512
-  static_assert((2 * kInts + (HB ? 4 : 2)) * B * kThreads / 2 + 2 * kWarps <= kPassScratch,
+  // layout in doubles: kInts x B x kThreads (int32 streams, both stages), 2 x B x
+  // kThreads per f64 stream, then the 2 x kWarps barriers
+  static_assert((kInts + (HB ? 4 : 2)) * B * kThreads + 2 * kWarps <= kPassScratch,
                 "SELL stages exceed the pass scratch");
   const DevPairs& I = P.I;
   const int lane = c.lane, warp = c.warp;
@@ -1346,6 +1349,143 @@ struct RowSrc {
   }
 };
 
+// Map pass of matrix-completion instances on the SELL copy (fast mode, one
+// GPU).  Every pair constraint k is an upper entry of its row i_k < n1, and
+// those rows fill the leading I.s_up_slices slices.  A warp owns one slice
+// (global warp index, round robin over every CTA of the team), lane = row a:
+// U_a is loaded once per row, the (column, multiplier, right-hand side)
+// streams arrive by TMA bulk copies exactly as in row_pass_sell_async, and a
+// constraint costs ONE gathered row instead of the edge-order pass's two plus
+// its row-index stream.  d_k = sum_c U(i_k,c) U(j_k,c) in column order, so
+// d_k and r_k are bit-identical to the edge-order pass (instances.cpp:27-35);
+// only the order in which the per-thread partials p.r and r.r are formed
+// differs (a fast-mode reduction order).  Ps: multiplier in SELL order, or
+// null (r.r only).
+template <int S, class UA>
+__device__ __forceinline__ void map_pass_sell(Ctx& c, const Params& P, const UA& U,
+                                              const double* __restrict__ Ps, double (&sums)[2]) {
+  constexpr int B = 6;
+  constexpr int kStageInts = B * 32;
+  static_assert((1 + 4) * B * kThreads + 2 * kWarps <= kPassScratch, "map stages exceed the pass scratch");
+  const DevPairs& I = P.I;
+  const int lane = c.lane, warp = c.warp;
+  int32_t* const colW = reinterpret_cast<int32_t*>(c.tw) + warp * 2 * kStageInts;
+  double* const pW = c.tw + B * kThreads + warp * 2 * kStageInts;
+  double* const bW = c.tw + 3 * B * kThreads + warp * 2 * kStageInts;
+  unsigned long long* const bar = reinterpret_cast<unsigned long long*>(c.tw + 5 * B * kThreads) + warp * 2;
+  const bool hp = Ps != nullptr;
+  const int64_t nsl = I.s_up_slices;
+  const int64_t gstride = (int64_t)c.t.size * kWarps;
+  struct Sl {
+    int64_t a, s_beg;
+    int L, nv, nlo;
+  };
+  auto slice = [&](int64_t sl) {
+    Sl x;
+    x.a = (sl << 5) + lane;
+    const bool mine = x.a < I.n;
+    x.s_beg = __ldg(I.s_off + sl);
+    x.L = (int)((__ldg(I.s_off + sl + 1) - x.s_beg) >> 5);
+    x.nv = mine ? __ldg(I.s_nv + x.a) : 0;
+    x.nlo = mine ? __ldg(I.s_nlo + x.a) : 0;
+    return x;
+  };
+  const unsigned long long pol = l2_evict_first();
+  auto issue = [&](int st, const Sl& x, int v0) {  // lane 0 only
+    const int ne = min(B, x.L - v0) * 32;
+    const int64_t g = x.s_beg + (int64_t)v0 * 32;
+    mbar_expect_tx(bar + st, (unsigned)ne * (hp ? 20u : 12u));
+    tma_load_1d(colW + st * kStageInts, I.s_col + g, ne * 4, bar + st, pol);
+    if (hp) tma_load_1d(pW + st * kStageInts, Ps + g, ne * 8, bar + st, pol);
+    tma_load_1d(bW + st * kStageInts, I.s_b + g, ne * 8, bar + st, pol);
+  };
+  int64_t sl = (int64_t)c.t.rank * kWarps + warp;
+  if (sl < nsl) {
+    if (lane == 0) {
+      mbar_init(bar, 1);
+      mbar_init(bar + 1, 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+    Sl X = slice(sl);
+    int st = 0;
+    unsigned phase = 0;
+    if (lane == 0 && X.L > 0) issue(0, X, 0);
+    while (true) {
+      double ua[S];
+      if (X.nv > X.nlo) {
+        sell_row<S>(U, X.a, ua);
+      } else {
+#pragma unroll
+        for (int k = 0; k < S; ++k) ua[k] = 0.0;
+      }
+      const int64_t sln = sl + gstride;
+      const bool have_next = sln < nsl;
+      Sl XN{};
+      if (have_next) XN = slice(sln);
+#pragma unroll 1
+      for (int v0 = 0; v0 < X.L; v0 += B) {
+        if (lane == 0) {
+          if (v0 + B < X.L)
+            issue(st ^ 1, X, v0 + B);
+          else if (have_next && XN.L > 0)
+            issue(st ^ 1, XN, 0);
+        }
+        mbar_wait(bar + st, (phase >> st) & 1u);
+        phase ^= 1u << st;
+        int32_t bc[B];
+        double pk[B], bk[B];
+#pragma unroll
+        for (int u = 0; u < B; ++u) {
+          const int v = v0 + u;
+          const bool ok = v < X.nv && v >= X.nlo;
+          bc[u] = ok ? colW[st * kStageInts + u * 32 + lane] : 0;
+          pk[u] = (ok && hp) ? pW[st * kStageInts + u * 32 + lane] : 0.0;
+          bk[u] = ok ? bW[st * kStageInts + u * 32 + lane] : 0.0;
+        }
+        __syncwarp();  // stage st is refilled by the next-but-one issue
+        double ub[B][S];
+#pragma unroll
+        for (int u = 0; u < B; ++u) {
+          const int v = v0 + u;
+          if (v < X.nv && v >= X.nlo) {
+            sell_row<S>(U, bc[u], ub[u]);
+          } else {
+#pragma unroll
+            for (int k = 0; k < S; ++k) ub[u][k] = 0.0;
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < B; ++u) {
+          const int v = v0 + u;
+          if (v >= X.nv) break;
+          if (v < X.nlo) continue;
+          double d = 0.0;
+#pragma unroll
+          for (int k = 0; k < S; ++k) {
+            const double tt = ua[k] * ub[u][k];
+            d = (k == 0) ? tt : d + tt;
+          }
+          const double r = d - bk[u];
+          if (hp) sums[0] = sums[0] + pk[u] * r;
+          sums[1] = sums[1] + r * r;
+        }
+        st ^= 1;
+      }
+      if (!have_next) break;
+      if (X.L == 0 && lane == 0 && XN.L > 0) issue(st, XN, 0);  // nothing was prefetched
+      sl = sln;
+      X = XN;
+    }
+    __syncwarp();
+    if (lane == 0) {
+      mbar_inval(bar);
+      mbar_inval(bar + 1);
+    }
+  }
+  __syncthreads();
+}
+
 template <int S>
 __device__ __forceinline__ void map_pass_src(Ctx& c, const Params& P, const RowSrc src, int s_rt,
                                           int mode, const double* __restrict__ pup, double* out,
@@ -1363,6 +1503,22 @@ __device__ __forceinline__ void map_pass_src(Ctx& c, const Params& P, const RowS
     }
   }
   const bool padded = S == 3 && I.s_col && P.pad;
+  if constexpr (S >= 1 && S <= 4) {
+    // matrix completion, one GPU: the row-ordered pass over the SELL copy
+    if ((mode == kMapPR || mode == kMapRR) && I.s_col && I.s_b && I.s_up_slices > 0) {
+      const double* Ps = mode == kMapPR ? sell_of(P, pup) : nullptr;
+      if (mode == kMapRR || Ps) {
+        if (padded) {
+          map_pass_sell<S>(c, P, UPad4{P.pad}, Ps, sums);
+          return;
+        }
+        if (src.U && sell_aligned<S>(src.U)) {
+          map_pass_sell<S>(c, P, UPlain{src.U}, Ps, sums);
+          return;
+        }
+      }
+    }
+  }
   for (int64_t k0 = c.kl + threadIdx.x; k0 < c.kh; k0 += (int64_t)kThreads * kUnroll) {
     int64_t ii[kUnroll], jj[kUnroll];
     double pk[kUnroll], bk[kUnroll], rf[kUnroll];

@@ -78,8 +78,37 @@ __device__ __forceinline__ void setup_ctx(Ctx& c, const Params& P, unsigned char
     c.rl = P.I.n * c.t.rank / c.t.size;
     c.rh = P.I.n * (c.t.rank + 1) / c.t.size;
   } else {
-    c.tl = P.I.ntiles * c.t.rank / c.t.size;
-    c.th = P.I.ntiles * (c.t.rank + 1) / c.t.size;
+    if (P.I.split_w >= 0 && P.fab.world == 1) {
+      // cost-balanced split: CTA r starts at the first tile whose prefix cost
+      // (entries of both CSR halves + split_w per row) reaches r/size of the
+      // total.  Equal tile counts leave CTAs of short-row regions with up to 2x
+      // the rows and 1.3x the entries of others at matrix completion (tiles cap
+      // at 512 entries), and every pass ends at a team barrier.
+      const int64_t* tr = P.I.tile_row;
+      const int64_t nt = P.I.ntiles, w = P.I.split_w;
+      auto cost = [&](int64_t t) {
+        const int64_t r = tr[t];
+        return P.I.up_ptr[r] + P.I.lo_ptr[r] + w * r;
+      };
+      const int64_t total = cost(nt);
+      auto first_at = [&](int rank) -> int64_t {
+        if (rank <= 0) return 0;
+        if (rank >= c.t.size) return nt;
+        const int64_t target = (int64_t)((__int128)total * rank / c.t.size);
+        int64_t lo = 0, hi = nt;  // smallest t with cost(t) >= target
+        while (lo < hi) {
+          const int64_t mid = (lo + hi) >> 1;
+          if (cost(mid) < target) lo = mid + 1;
+          else hi = mid;
+        }
+        return lo;
+      };
+      c.tl = first_at(c.t.rank);
+      c.th = first_at(c.t.rank + 1);
+    } else {
+      c.tl = P.I.ntiles * c.t.rank / c.t.size;
+      c.th = P.I.ntiles * (c.t.rank + 1) / c.t.size;
+    }
     c.rl = P.I.tile_row[c.tl];
     c.rh = P.I.tile_row[c.th];
   }

@@ -86,3 +86,36 @@ def test_matcomp_c4_full_size(H):
     rng = np.random.default_rng(4)
     U = rng.standard_normal((inst.n, 3)) / np.sqrt(inst.n)
     _check_operator_properties(inst, U, i, j + 400000, False, rng)
+
+
+def test_matcomp_c4_al_value_row_ordered_map(H):
+    """al_value at C4 runs the row-ordered SELL map pass (one gathered row per
+    constraint, device.cuh map_pass_sell): r_k is bit-identical to the edge-order
+    map, only the partial sums p.r and r.r are formed in another order, so the
+    value matches the reference formula (sdp_instance.cpp:50-60) to 1e-12."""
+    spec = H.McSpec(400000, 600000, 3, seed=0)
+    inst = H.gen_matrix_completion(spec)
+    rng = np.random.default_rng(5)
+    U = rng.standard_normal((inst.n, 3)) / np.sqrt(inst.n)
+    p = rng.standard_normal(inst.m)
+    beta = 7.0
+    r = inst.apply_map(U) - inst.b
+    ref = 0.5 * float(np.sum(U * U)) + float(p @ r) + 0.5 * beta * float(r @ r)
+    val = inst.al_value(U, p, beta)
+    assert val == pytest.approx(ref, rel=1e-12)
+
+
+def test_matcomp_solve_row_ordered_map_vs_edge_order(H, monkeypatch):
+    """The fast solve with the row-ordered map (default) and with the edge-order
+    map (CUHALLAR_NO_SELL_MAP=1, read at instance build) reach the same optimum:
+    status, rank and pval within 1e-6 (the two differ only in the order of the
+    map's partial sums)."""
+    spec = H.McSpec(100000, 150000, 3, seed=0)
+    inst = H.gen_matrix_completion(spec)
+    rep = H.solve(inst, H.SolverConfig(eps=1e-5))
+    monkeypatch.setenv("CUHALLAR_NO_SELL_MAP", "1")
+    inst2 = H.gen_matrix_completion(spec)
+    rep2 = H.solve(inst2, H.SolverConfig(eps=1e-5))
+    assert rep.status == rep2.status == "optimal"
+    assert rep.rank == rep2.rank == 3
+    assert abs(rep.pval - rep2.pval) <= 1e-6 * abs(rep2.pval)

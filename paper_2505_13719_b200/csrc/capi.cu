@@ -202,7 +202,24 @@ struct cuhallar_solution {
   int64_t n = 0, m = 0;
   int rank = 0;
   std::vector<double> U;  // column-major
-  std::vector<double> p;
+  std::vector<double> p;  // host copy (sharded solves), empty when p_dev holds it
+  // single-GPU solves: a device copy of the pair multipliers (D2D at solve end)
+  // and the trace multiplier; cuhallar_solution_get_p copies straight into the
+  // caller's buffer (one D2H, no zero-filled 1 GB staging vector at C4)
+  double* p_dev = nullptr;
+  int64_t np = 0;
+  bool has_trace = false;
+  double p_trace = 0.0;
+  int device = 0;
+  ~cuhallar_solution() {
+    if (p_dev) {
+      int cur = 0;
+      cudaGetDevice(&cur);
+      cudaSetDevice(device);
+      cudaFree(p_dev);
+      cudaSetDevice(cur);
+    }
+  }
 };
 
 namespace {
@@ -261,6 +278,7 @@ void build_sell(cuhallar_instance* in) {
   // share of the row passes at C4 (profiles/r02/profile_c4_phases_final.jsonl)
   const char* et = std::getenv("CUHALLAR_EVEN_TILES");
   if (!(et && *et && *et != '0')) I.split_w = 64;
+  if (const char* ew = std::getenv("CUHALLAR_SPLIT_W")) I.split_w = std::max(0, std::atoi(ew));  // sweeps
   const char* em = std::getenv("CUHALLAR_NO_SELL_MAP");
   if (h.family == kMatcomp && !h.has_trace && h.np > 0 && in->s_b && !(em && *em && *em != '0')) {
     int32_t last = 0;
@@ -1392,12 +1410,16 @@ static int fill_report(cuhallar_instance* in, const SolveOut& so, float ms, doub
       S->U.resize(rm.size());
       for (int64_t a = 0; a < n; ++a)
         for (int k = 0; k < so.rank; ++k) S->U[a + k * n] = rm[a * so.rank + k];
-      S->p.resize(in->h.m);
       const int world = int(ranks.size());
       if (world == 1) {
-        ck(cudaMemcpy(S->p.data(), in->p_up, in->h.np * sizeof(double), cudaMemcpyDeviceToHost),
-           "p out");
+        S->np = in->h.np;
+        S->has_trace = in->h.has_trace != 0;
+        S->p_trace = so.p_trace;
+        S->device = in->device;
+        ck(cudaMalloc(&S->p_dev, std::max<int64_t>(1, in->h.np) * sizeof(double)), "p out");
+        ck(cudaMemcpy(S->p_dev, in->p_up, in->h.np * sizeof(double), cudaMemcpyDeviceToDevice), "p out");
       } else {
+        S->p.resize(in->h.m);
         const int64_t nt = int64_t(in->tile_row_host.size()) - 1;
         for (int r = 0; r < world; ++r) {
           const int64_t rl = in->tile_row_host[nt * r / world];
@@ -1410,7 +1432,7 @@ static int fill_report(cuhallar_instance* in, const SolveOut& so, float ms, doub
                "p out");
         }
       }
-      if (in->h.has_trace) S->p[in->h.np] = so.p_trace;
+      if (in->h.has_trace && world > 1) S->p[in->h.np] = so.p_trace;
       *sol = S.release();
     }
     return 0;
@@ -1685,8 +1707,16 @@ int cuhallar_solution_get_U(const cuhallar_solution* s, double* U) {
   return 0;
 }
 int cuhallar_solution_get_p(const cuhallar_solution* s, double* p) {
-  std::memcpy(p, s->p.data(), s->p.size() * sizeof(double));
-  return 0;
+  return guard([&] {
+    if (s->p_dev) {
+      DevGuard dg(s->device);
+      ck(cudaMemcpy(p, s->p_dev, s->np * sizeof(double), cudaMemcpyDeviceToHost), "p out");
+      if (s->has_trace) p[s->np] = s->p_trace;
+    } else {
+      std::memcpy(p, s->p.data(), s->p.size() * sizeof(double));
+    }
+    return 0;
+  });
 }
 void cuhallar_solution_destroy(cuhallar_solution* s) { delete s; }
 

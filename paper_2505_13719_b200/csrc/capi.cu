@@ -273,11 +273,11 @@ void build_sell(cuhallar_instance* in) {
   // every upper entry -> the row-ordered map pass (device.cuh map_pass_sell);
   // CUHALLAR_NO_SELL_MAP=1 keeps the edge-order map (A/B runs)
   // cost-balanced CTA row split (kernel_setup.cuh); CUHALLAR_EVEN_TILES=1
-  // keeps equal tile counts (A/B runs).  64 entries per row: a row's share of
-  // the row-wise passes (CGS2, BLAS-1, epilogues) measured against an entry's
-  // share of the row passes at C4 (profiles/r02/profile_c4_phases_final.jsonl)
+  // keeps equal tile counts (A/B runs).  32 entries per row: the C4 solve
+  // measured 3.27 / 3.26 / 3.41 / 3.43 s at 16 / 32 / 64 / 128 per row and
+  // 3.77 s with equal tile counts (profiles/r02/ab_s4)
   const char* et = std::getenv("CUHALLAR_EVEN_TILES");
-  if (!(et && *et && *et != '0')) I.split_w = 64;
+  if (!(et && *et && *et != '0')) I.split_w = 32;
   if (const char* ew = std::getenv("CUHALLAR_SPLIT_W")) I.split_w = std::max(0, std::atoi(ew));  // sweeps
   const char* em = std::getenv("CUHALLAR_NO_SELL_MAP");
   if (h.family == kMatcomp && !h.has_trace && h.np > 0 && in->s_b && !(em && *em && *em != '0')) {
@@ -285,6 +285,10 @@ void build_sell(cuhallar_instance* in) {
     ck(cudaMemcpy(&last, in->ei + (h.np - 1), sizeof(int32_t), cudaMemcpyDeviceToHost), "ei tail");
     I.s_up_slices = (int64_t(last) + 32) / 32;
   }
+  // theta: upper entries in every slice; worth it while the SELL padding is
+  // small (uniform degrees, e.g. hypercubes: s_slots == 2 np)
+  if (h.has_trace && h.np > 0 && slots <= 2 * h.np + h.np / 2 && !(em && *em && *em != '0'))
+    I.s_up_slices = sl.nslices;
 }
 
 // Device structure of a pair instance (devgen.cu builds it on the GPU):

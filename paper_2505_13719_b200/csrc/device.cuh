@@ -1349,9 +1349,10 @@ struct RowSrc {
   }
 };
 
-// Map pass of matrix-completion instances on the SELL copy (fast mode, one
-// GPU).  Every pair constraint k is an upper entry of its row i_k < n1, and
-// those rows fill the leading I.s_up_slices slices.  A warp owns one slice
+// Map pass on the SELL copy (fast mode, one GPU).  Every pair constraint k is
+// the upper entry of row i_k; the slices [0, I.s_up_slices) hold all of them
+// (matrix completion: the rows i_k < n1; theta: every slice, entries below
+// the slice's smallest lower-entry count are not streamed).  A warp owns one slice
 // (global warp index, round robin over every CTA of the team), lane = row a:
 // U_a is loaded once per row, the (column, multiplier, right-hand side)
 // streams arrive by TMA bulk copies exactly as in row_pass_sell_async, and a
@@ -1374,13 +1375,14 @@ __device__ __forceinline__ void map_pass_sell(Ctx& c, const Params& P, const UA&
   double* const bW = c.tw + 3 * B * kThreads + warp * 2 * kStageInts;
   unsigned long long* const bar = reinterpret_cast<unsigned long long*>(c.tw + 5 * B * kThreads) + warp * 2;
   const bool hp = Ps != nullptr;
+  const bool hb = I.s_b != nullptr;  // theta: b = 0 on the pairs
   const int64_t nsl = I.s_up_slices;
   const int64_t gstride = (int64_t)c.t.size * kWarps;
   struct Sl {
     int64_t a, s_beg;
-    int L, nv, nlo;
+    int L, nv, nlo, vs;  // vs: first entry any lane needs (warp-uniform)
   };
-  auto slice = [&](int64_t sl) {
+  auto slice = [&](int64_t sl) {  // warp-collective
     Sl x;
     x.a = (sl << 5) + lane;
     const bool mine = x.a < I.n;
@@ -1388,16 +1390,21 @@ __device__ __forceinline__ void map_pass_sell(Ctx& c, const Params& P, const UA&
     x.L = (int)((__ldg(I.s_off + sl + 1) - x.s_beg) >> 5);
     x.nv = mine ? __ldg(I.s_nv + x.a) : 0;
     x.nlo = mine ? __ldg(I.s_nlo + x.a) : 0;
+    // lower entries come first in every row: entries below the smallest nlo
+    // of the slice's rows (that have upper entries) are not streamed
+    const unsigned cand = x.nv > x.nlo ? (unsigned)x.nlo : 0x7fffffffu;
+    const unsigned vs = __reduce_min_sync(0xffffffffu, cand);
+    x.vs = vs == 0x7fffffffu ? x.L : (int)vs;
     return x;
   };
   const unsigned long long pol = l2_evict_first();
   auto issue = [&](int st, const Sl& x, int v0) {  // lane 0 only
     const int ne = min(B, x.L - v0) * 32;
     const int64_t g = x.s_beg + (int64_t)v0 * 32;
-    mbar_expect_tx(bar + st, (unsigned)ne * (hp ? 20u : 12u));
+    mbar_expect_tx(bar + st, (unsigned)ne * (4u + (hp ? 8u : 0u) + (hb ? 8u : 0u)));
     tma_load_1d(colW + st * kStageInts, I.s_col + g, ne * 4, bar + st, pol);
     if (hp) tma_load_1d(pW + st * kStageInts, Ps + g, ne * 8, bar + st, pol);
-    tma_load_1d(bW + st * kStageInts, I.s_b + g, ne * 8, bar + st, pol);
+    if (hb) tma_load_1d(bW + st * kStageInts, I.s_b + g, ne * 8, bar + st, pol);
   };
   int64_t sl = (int64_t)c.t.rank * kWarps + warp;
   if (sl < nsl) {
@@ -1410,7 +1417,7 @@ __device__ __forceinline__ void map_pass_sell(Ctx& c, const Params& P, const UA&
     Sl X = slice(sl);
     int st = 0;
     unsigned phase = 0;
-    if (lane == 0 && X.L > 0) issue(0, X, 0);
+    if (lane == 0 && X.vs < X.L) issue(0, X, X.vs);
     while (true) {
       double ua[S];
       if (X.nv > X.nlo) {
@@ -1424,12 +1431,12 @@ __device__ __forceinline__ void map_pass_sell(Ctx& c, const Params& P, const UA&
       Sl XN{};
       if (have_next) XN = slice(sln);
 #pragma unroll 1
-      for (int v0 = 0; v0 < X.L; v0 += B) {
+      for (int v0 = X.vs; v0 < X.L; v0 += B) {
         if (lane == 0) {
           if (v0 + B < X.L)
             issue(st ^ 1, X, v0 + B);
-          else if (have_next && XN.L > 0)
-            issue(st ^ 1, XN, 0);
+          else if (have_next && XN.vs < XN.L)
+            issue(st ^ 1, XN, XN.vs);
         }
         mbar_wait(bar + st, (phase >> st) & 1u);
         phase ^= 1u << st;
@@ -1441,7 +1448,7 @@ __device__ __forceinline__ void map_pass_sell(Ctx& c, const Params& P, const UA&
           const bool ok = v < X.nv && v >= X.nlo;
           bc[u] = ok ? colW[st * kStageInts + u * 32 + lane] : 0;
           pk[u] = (ok && hp) ? pW[st * kStageInts + u * 32 + lane] : 0.0;
-          bk[u] = ok ? bW[st * kStageInts + u * 32 + lane] : 0.0;
+          bk[u] = (ok && hb) ? bW[st * kStageInts + u * 32 + lane] : 0.0;
         }
         __syncwarp();  // stage st is refilled by the next-but-one issue
         double ub[B][S];
@@ -1473,7 +1480,7 @@ __device__ __forceinline__ void map_pass_sell(Ctx& c, const Params& P, const UA&
         st ^= 1;
       }
       if (!have_next) break;
-      if (X.L == 0 && lane == 0 && XN.L > 0) issue(st, XN, 0);  // nothing was prefetched
+      if (X.vs >= X.L && lane == 0 && XN.vs < XN.L) issue(st, XN, XN.vs);  // nothing was prefetched
       sl = sln;
       X = XN;
     }
@@ -1504,8 +1511,9 @@ __device__ __forceinline__ void map_pass_src(Ctx& c, const Params& P, const RowS
   }
   const bool padded = S == 3 && I.s_col && P.pad;
   if constexpr (S >= 1 && S <= 4) {
-    // matrix completion, one GPU: the row-ordered pass over the SELL copy
-    if ((mode == kMapPR || mode == kMapRR) && I.s_col && I.s_b && I.s_up_slices > 0) {
+    // one GPU (matrix completion; theta with little SELL padding): the
+    // row-ordered pass over the SELL copy
+    if ((mode == kMapPR || mode == kMapRR) && I.s_col && I.s_up_slices > 0) {
       const double* Ps = mode == kMapPR ? sell_of(P, pup) : nullptr;
       if (mode == kMapRR || Ps) {
         if (padded) {

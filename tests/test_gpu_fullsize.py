@@ -119,3 +119,25 @@ def test_matcomp_solve_row_ordered_map_vs_edge_order(H, monkeypatch):
     assert rep.status == rep2.status == "optimal"
     assert rep.rank == rep2.rank == 3
     assert abs(rep.pval - rep2.pval) <= 1e-6 * abs(rep2.pval)
+
+
+@pytest.mark.parametrize("d", [18, 23])
+def test_hamming_al_value_row_ordered_map(H, d, monkeypatch):
+    """Theta on a hypercube (uniform degree, no SELL padding) runs the
+    row-ordered SELL map too (upper entries of every slice, the lower prefix
+    skipped): al_value equals the reference formula cdot + p.r + beta/2 |r|^2
+    (sdp_instance.cpp:50-60) to 1e-12 and the edge-order map's value
+    (CUHALLAR_NO_SELL_MAP=1) to 1e-12."""
+    inst = H.build_theta_instance(H.make_hypercube(d))
+    rng = np.random.default_rng(d)
+    U = rng.standard_normal((inst.n, 2)) / np.sqrt(inst.n)
+    p = rng.standard_normal(inst.m)
+    beta = 5.0
+    r = inst.apply_map(U) - inst.b
+    ref = float(np.sum(inst.apply_C(U) * U)) + float(p @ r) + 0.5 * beta * float(r @ r)
+    val = inst.al_value(U, p, beta)
+    assert val == pytest.approx(ref, rel=1e-12)
+    del inst
+    monkeypatch.setenv("CUHALLAR_NO_SELL_MAP", "1")
+    inst2 = H.build_theta_instance(H.make_hypercube(d))
+    assert inst2.al_value(U, p, beta) == pytest.approx(val, rel=1e-12)

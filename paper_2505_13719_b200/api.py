@@ -21,6 +21,7 @@ from __future__ import annotations
 
 import ctypes as C
 import os
+import warnings
 from dataclasses import dataclass, field
 from typing import Callable, Optional
 
@@ -605,6 +606,9 @@ def solve(inst: SdpInstance, cfg: SolverConfig = None, U0=None, p0=None,
     r = _report(inst, rep, sol, fetch)
     if sink is not None:
         r.trace = events
+        if rep.trace_dropped > 0:  # the device ring overflowed: the sink missed events
+            warnings.warn(f"solve: {rep.trace_dropped} trace events were dropped (device trace ring full)",
+                          RuntimeWarning, stacklevel=2)
     return r
 
 

@@ -141,3 +141,33 @@ def test_hamming_al_value_row_ordered_map(H, d, monkeypatch):
     monkeypatch.setenv("CUHALLAR_NO_SELL_MAP", "1")
     inst2 = H.build_theta_instance(H.make_hypercube(d))
     assert inst2.al_value(U, p, beta) == pytest.approx(val, rel=1e-12)
+
+
+def test_circulant_theta_al_value_row_ordered_map(H, monkeypatch):
+    """A uniform-degree graph that is not a hypercube (circulant, offsets
+    1, 5, 77, 1000, 54321: degree 10, lower-entry counts that vary across each
+    SELL slice near the wrap-around) takes the row-ordered theta map with the
+    lower-prefix skip: al_value equals the reference formula and the
+    edge-order map's value to 1e-12."""
+    n = 1 << 18
+    u = np.arange(n, dtype=np.int64)
+    e = []
+    for off in (1, 5, 77, 1000, 54321):
+        v = (u + off) % n
+        e.append(np.stack([np.minimum(u, v), np.maximum(u, v)], axis=1))
+    edges = np.unique(np.concatenate(e), axis=0)
+    g = H.graph_from_edges(n, edges)
+    inst = H.build_theta_instance(g)
+    assert inst.m == len(edges) + 1
+    rng = np.random.default_rng(11)
+    U = rng.standard_normal((n, 2)) / np.sqrt(n)
+    p = rng.standard_normal(inst.m)
+    beta = 3.0
+    r = inst.apply_map(U) - inst.b
+    ref = float(np.sum(inst.apply_C(U) * U)) + float(p @ r) + 0.5 * beta * float(r @ r)
+    val = inst.al_value(U, p, beta)
+    assert val == pytest.approx(ref, rel=1e-12)
+    del inst
+    monkeypatch.setenv("CUHALLAR_NO_SELL_MAP", "1")
+    inst2 = H.build_theta_instance(H.graph_from_edges(n, edges))
+    assert inst2.al_value(U, p, beta) == pytest.approx(val, rel=1e-12)

@@ -36,6 +36,20 @@ def _make(H, name):
     raise KeyError(name)
 
 
+def _oracle(orc, name):
+    if name == "C5":
+        return orc.OracleInstance.cycle(5)
+    if name == "petersen":
+        return orc.OracleInstance.petersen()
+    if name.startswith("H"):
+        return orc.OracleInstance.hypercube(int(name[1:]))
+    if name == "mc100":
+        return orc.OracleInstance.matcomp(100, 210, 3, seed=0)
+    if name == "mc2000":
+        return orc.OracleInstance.matcomp(2000, 2000, 3, seed=0)
+    raise KeyError(name)
+
+
 def test_world1_is_the_plain_solve(H):
     a = H.solve(_make(H, "H6"))
     b = H.solve_sharded([_make(H, "H6")])
@@ -54,6 +68,10 @@ def test_sharded_theta(H, orc, name, value, relative, world):
     err = abs(-rep.pval - value) / (value if relative else 1.0)
     assert err <= 1e-4
     assert abs(rep.pval - single.pval) <= 1e-6 * max(1.0, abs(single.pval))
+    # against the CPU oracle's own solve of the same instance (final objective <= 1e-6)
+    o = _oracle(orc, name).solve()
+    assert o.status == "optimal"
+    assert abs(rep.pval - o.pval) <= 1e-6 * max(1.0, abs(o.pval))
     assert max(rep.rel_pfeas, rep.rel_gap, rep.rel_dfeas) <= 1e-5
     assert rep.U.shape == (insts[0].n, rep.rank) and rep.p.shape == (insts[0].m,)
     # the returned (U, p) is a certified point: warm start finishes in one outer iteration
@@ -69,6 +87,9 @@ def test_sharded_matcomp(H, orc, name):
     assert rep.status == "optimal" and rep.rank == single.rank
     assert abs(rep.pval - single.pval) <= 1e-6 * abs(single.pval)
     assert abs(rep.pval - insts[0].nuclear_norm) / insts[0].nuclear_norm <= 1e-3
+    o = _oracle(orc, name).solve()
+    assert o.status == "optimal" and o.rank == rep.rank
+    assert abs(rep.pval - o.pval) <= 1e-6 * abs(o.pval)
 
 
 def test_sharded_deterministic(H):
